@@ -1,0 +1,201 @@
+/*
+ * gemmguard_b200.h — C-ABI of the B200-native checksum-protected GEMM path.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `gemmguard` (/root/reference/pkg/src/gemmguard).  The reference has no FFI
+ * of its own: its interface is the Python module API.  Each entry point below
+ * replaces one reference function (cited file:line); the Python host package
+ * `paper_2310_03841_b200` binds them through ctypes and keeps the reference's
+ * names, signatures and exceptions.
+ *
+ * Conventions (all entry points):
+ *   - every pointer argument is a DEVICE pointer unless the parameter name
+ *     ends in `_host`;
+ *   - every call takes a cudaStream_t (passed as void*) and is asynchronous on
+ *     it; there are no hidden device synchronisations and no allocations —
+ *     the caller owns all memory, including workspace;
+ *   - return 0 on success, a negative GG_E* code on failure; the message of
+ *     the last failure on the calling thread is `gg_last_error()`;
+ *   - re-entrant per stream (workspace must not be shared by concurrent calls).
+ */
+#ifndef GEMMGUARD_B200_H
+#define GEMMGUARD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GG_API __attribute__((visibility("default")))
+#else
+#define GG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- element types (reference dtype tags: numerics.py:31-37) ------------ */
+enum gg_dtype {
+  GG_F64 = 0,   /* "binary64"                                              */
+  GG_F32 = 1,   /* "binary32"  (tensor path: kind::tf32)                   */
+  GG_F16 = 2,   /* "binary16-emulated" (stored as real fp16 on device)     */
+  GG_BF16 = 3,  /* extension: bfloat16 (fields 7,8) — not in the reference */
+  GG_I8 = 4,    /* "int8"                                                  */
+  GG_I32 = 5,   /* "int32"                                                 */
+  GG_I64 = 6
+};
+
+/* ---- checksum / accumulation precisions (numerics.py:77-111) ------------ */
+enum gg_precision {
+  GG_P_F16 = 0, /* Precision.BINARY16  "binary16-emulated" */
+  GG_P_F32 = 1, /* Precision.BINARY32  */
+  GG_P_F64 = 2, /* Precision.BINARY64  */
+  GG_P_I64 = 3  /* Precision.INT64     "int64-exact" */
+};
+
+enum gg_statistic { GG_PER_SAMPLE = 0, GG_BATCH_MEAN = 1 };    /* guard.py:93  */
+enum gg_inj_target { GG_INJ_OUTPUT = 0, GG_INJ_ACCUMULATOR = 1 };
+enum gg_inj_mode { GG_INJ_BITFLIP = 0, GG_INJ_SET_VALUE = 1 }; /* injector.py:49-50 */
+
+enum gg_error {
+  GG_OK = 0,
+  GG_EINVAL = -1,     /* bad argument (shape, dtype, alignment, domain)   */
+  GG_ECUDA = -2,      /* CUDA runtime / driver failure                    */
+  GG_EWORKSPACE = -3, /* workspace too small                              */
+  GG_EUNSUPPORTED = -4
+};
+
+/* One fault to inject inside the protected GEMM epilogue.
+ * target OUTPUT flips bit `bit` of the stored encoding of C[row, col] (or
+ * replaces it by `value` rounded to the output type) after bias add and
+ * rounding, before the observed checksum — injector.py:265-271 /
+ * guard.py:515-523.  target ACCUMULATOR flips the raw fp32/s32 TMEM
+ * accumulator before the bias add (build extension). */
+typedef struct gg_injection {
+  int64_t row;
+  int32_t col;
+  int32_t bit;
+  int32_t target; /* gg_inj_target */
+  int32_t mode;   /* gg_inj_mode   */
+  double value;   /* used when mode == GG_INJ_SET_VALUE */
+} gg_injection;
+
+/* Descriptor of one protected GEMM launch:
+ *     C[m, n] = sum_k A[m, k] * B[n, k] + bias[n]
+ * A is the layer input X [M, K] row-major; B is the weight in torch layout
+ * W [N, K] row-major (K-major), i.e. the transpose of the reference's stored
+ * Wt [K, N] (model.py:43).  With protect=1 the epilogue also produces the
+ * per-row discrepancy d[m] = (sum_k A[m,k]*w_sum[k] + bias_sum) - sum_n C[m,n]
+ * over the STORED (rounded, bias-included, possibly injected) outputs, the
+ * flags and the summary scalars of guard._verify_arrays (guard.py:188-215). */
+typedef struct gg_gemm_desc {
+  int32_t ab_kind;  /* GG_BF16 | GG_F16 | GG_F32 (tf32 MMA) | GG_I8       */
+  int32_t c_dtype;  /* float kinds: GG_BF16 | GG_F16 | GG_F32; GG_I8: GG_I32 */
+  int64_t M, N, K;
+  const void* A; int64_t lda; /* elements; lda*size % 16 == 0, A 16B aligned */
+  const void* B; int64_t ldb; /* elements; ldb*size % 16 == 0, B 16B aligned */
+  const void* bias;           /* [N] f32 (float kinds) or i32 (GG_I8); NULL = 0 */
+  void* C; int64_t ldc;       /* elements */
+
+  int32_t protect;            /* 0: unprotected baseline of the same kernel  */
+  int32_t chk_prec;           /* GG_P_F64 (float kinds) or GG_P_I64 (GG_I8)  */
+  const void* w_sum;          /* [K] f64 or i64: gg_offline_checksum output  */
+  double bias_sum_f;          /* bias_sum for GG_P_F64                       */
+  int64_t bias_sum_i;         /* bias_sum for GG_P_I64                       */
+  double mu, lo, hi;          /* EpsilonModel mu, threshold_low/high         */
+  int32_t statistic;          /* gg_statistic                                */
+
+  void* d;                    /* [M] f64 (GG_P_F64) or i64 (GG_P_I64)        */
+  uint8_t* flags;             /* [M] 0/1                                     */
+  double* max_disc;           /* scalar                                      */
+  int32_t* nflag;             /* scalar: number of flagged rows              */
+  uint8_t* triggered;         /* scalar 0/1                                  */
+
+  const gg_injection* inj;    /* device array, may be NULL                   */
+  int32_t n_inj;
+
+  void* workspace;            /* zero-filled before first use; every call    */
+  size_t workspace_bytes;     /* leaves it zero-filled again on completion   */
+
+  /* replay (gg_replay_tiles only): */
+  const uint8_t* replay_rows; /* [M] rows whose M-bands are recomputed       */
+  int32_t* changed;           /* scalar: outputs whose bytes changed         */
+} gg_gemm_desc;
+
+/* Library identity. */
+GG_API const char* gg_last_error(void);
+GG_API int gg_version(void);
+
+/* Bytes of workspace gg_protected_gemm / gg_replay_tiles need for (M, N). */
+GG_API size_t gg_protected_gemm_workspace_bytes(int64_t M, int64_t N);
+
+/* K1 — protected GEMM (tcgen05 + TMEM + TMA, sm_100a).
+ * Replaces numerics.gemm (numerics.py:237-289) + model.run_layer
+ * (model.py:334-338) + guard._discrepancies (guard.py:163-171) +
+ * guard._verify_arrays (guard.py:188-215) fused in one launch. */
+GG_API int gg_protected_gemm(const gg_gemm_desc* desc, void* stream);
+
+/* K4 — replay only the M-bands holding a row with replay_rows[m] != 0, with
+ * the identical tile configuration and K order as gg_protected_gemm, writing
+ * the recomputed tiles into C, counting outputs whose bytes changed into
+ * *changed, and re-deriving d/flags/summaries over all rows.
+ * Replaces guard._replay (guard.py:575-604). */
+GG_API int gg_replay_tiles(const gg_gemm_desc* desc, void* stream);
+
+/* K2 — offline weight checksum w_sum[k] = sum_n W[n,k] (ascending n) and
+ * bias_sum = sum_n bias[n] in precision chk_prec; bit-exact with
+ * guard.offline_checksum (guard.py:142-160, _accumulate_in 135-139).
+ * w_layout 0: W is [N, K] row-major (torch); 1: W is Wt [K, N] (reference).
+ * w_sum_out: [K] of the precision's type (f16/f32/f64/i64);
+ * bias_sum_out: one element of that type.  bias may be NULL (sum = 0). */
+GG_API int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_t N,
+                        int64_t ldw, int32_t w_layout, const void* bias,
+                        int32_t bias_dtype, int32_t chk_prec, void* w_sum_out,
+                        void* bias_sum_out, void* stream);
+
+/* Reference-exact verification of a given (X, Y): sequential folds in the
+ * checksum precision exactly as guard._discrepancies (guard.py:163-171) and
+ * the flag/summary rules of guard._verify_arrays (guard.py:188-215).
+ * X [M, K] (ldx) of x_dtype, Y [M, N] (ldy) of y_dtype, w_sum [K] and
+ * bias_sum (one element) of the precision's type.  d_out is f64 for float
+ * precisions and i64 for GG_P_I64.  max_disc/nflag/triggered as above. */
+GG_API int gg_verify_rows(int32_t x_dtype, const void* X, int64_t M, int64_t K,
+                   int64_t ldx, int32_t y_dtype, const void* Y, int64_t N,
+                   int64_t ldy, int32_t chk_prec, const void* w_sum,
+                   const void* bias_sum, double mu, double lo, double hi,
+                   int32_t statistic, void* d_out, uint8_t* flags_out,
+                   double* max_disc_out, int32_t* nflag_out,
+                   uint8_t* triggered_out, void* stream);
+
+/* K3 — flip bit bit_idx[i] of element elem_idx[i] of the buffer `ptr` whose
+ * elements are elem_bytes wide (1, 2, 4 or 8), for i < n (device arrays).
+ * The flip is an involution: call twice to restore.  Replaces
+ * numerics.flip_bit (numerics.py:308-321) for operand/weight locations. */
+GG_API int gg_flip_bits(void* ptr, int32_t elem_bytes, const int64_t* elem_idx,
+                 const int32_t* bit_idx, int64_t n, void* stream);
+
+/* Reference-exact GEMM on CUDA cores: ascending-k single accumulator in the
+ * accumulation precision, products rounded before the add, result rounded to
+ * the operand dtype — bit-exact with numerics.gemm (numerics.py:222-289)
+ * for every (dtype, accum) pair the reference accepts.  Used for parity and
+ * as the binary64 path; the tensor path is gg_protected_gemm.
+ * X [M, K] row-major, Wt [K, N] row-major (reference layout), bias [N] of
+ * the accumulation type (or i32 for integers), Y [M, N] of the operand type
+ * (i32 for integer operands). */
+GG_API int gg_gemm_exact(int32_t dtype, int32_t accum, const void* X, int64_t M,
+                  int64_t K, const void* Wt, int64_t N, const void* bias,
+                  void* Y, void* stream);
+
+/* numerics.reduce_rows / reduce_cols (numerics.py:292-305): ascending f64
+ * (i64 for integer dtypes) folds; axis 1 = per row, axis 0 = per column. */
+GG_API int gg_reduce(int32_t dtype, const void* A, int64_t rows, int64_t cols,
+              int32_t axis, void* out, void* stream);
+
+/* Elementwise helpers used by the host package (all device arrays). */
+GG_API int gg_round_f64_to(int32_t dtype, const double* in, void* out, int64_t n,
+                    void* stream); /* RNE: numerics._round_array 202-208 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEMMGUARD_B200_H */

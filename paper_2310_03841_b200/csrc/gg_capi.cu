@@ -1,0 +1,81 @@
+// gg_capi.cu — extern "C" entry points declared in include/gemmguard_b200.h.
+// Plain pointers and sizes only; no torch types cross this boundary.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "gg_internal.h"
+
+namespace gg {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(GG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
+}  // namespace gg
+
+extern "C" {
+
+const char* gg_last_error(void) { return gg::g_last_error.c_str(); }
+
+int gg_version(void) { return 10000; }  // 1.0.0
+
+size_t gg_protected_gemm_workspace_bytes(int64_t M, int64_t N) {
+  if (M < 1 || N < 1) return 0;
+  return gg::protected_gemm_workspace_bytes(M, N);
+}
+
+int gg_protected_gemm(const gg_gemm_desc* desc, void* stream) {
+  return gg::launch_protected_gemm(desc, false, static_cast<cudaStream_t>(stream));
+}
+
+int gg_replay_tiles(const gg_gemm_desc* desc, void* stream) {
+  return gg::launch_protected_gemm(desc, true, static_cast<cudaStream_t>(stream));
+}
+
+int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_t N, int64_t ldw, int32_t w_layout,
+                        const void* bias, int32_t bias_dtype, int32_t chk_prec, void* w_sum_out,
+                        void* bias_sum_out, void* stream) {
+  return gg::launch_offline_checksum(w_dtype, W, K, N, ldw, w_layout, bias, bias_dtype, chk_prec, w_sum_out,
+                                     bias_sum_out, static_cast<cudaStream_t>(stream));
+}
+
+int gg_verify_rows(int32_t x_dtype, const void* X, int64_t M, int64_t K, int64_t ldx, int32_t y_dtype, const void* Y,
+                   int64_t N, int64_t ldy, int32_t chk_prec, const void* w_sum, const void* bias_sum, double mu,
+                   double lo, double hi, int32_t statistic, void* d_out, uint8_t* flags_out, double* max_disc_out,
+                   int32_t* nflag_out, uint8_t* triggered_out, void* stream) {
+  return gg::launch_verify_rows(x_dtype, X, M, K, ldx, y_dtype, Y, N, ldy, chk_prec, w_sum, bias_sum, mu, lo, hi,
+                                statistic, d_out, flags_out, max_disc_out, nflag_out, triggered_out,
+                                static_cast<cudaStream_t>(stream));
+}
+
+int gg_flip_bits(void* ptr, int32_t elem_bytes, const int64_t* elem_idx, const int32_t* bit_idx, int64_t n,
+                 void* stream) {
+  return gg::launch_flip_bits(ptr, elem_bytes, elem_idx, bit_idx, n, static_cast<cudaStream_t>(stream));
+}
+
+int gg_gemm_exact(int32_t dtype, int32_t accum, const void* X, int64_t M, int64_t K, const void* Wt, int64_t N,
+                  const void* bias, void* Y, void* stream) {
+  return gg::launch_gemm_exact(dtype, accum, X, M, K, Wt, N, bias, Y, static_cast<cudaStream_t>(stream));
+}
+
+int gg_reduce(int32_t dtype, const void* A, int64_t rows, int64_t cols, int32_t axis, void* out, void* stream) {
+  return gg::launch_reduce(dtype, A, rows, cols, axis, out, static_cast<cudaStream_t>(stream));
+}
+
+int gg_round_f64_to(int32_t dtype, const double* in, void* out, int64_t n, void* stream) {
+  return gg::launch_round(dtype, in, out, n, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

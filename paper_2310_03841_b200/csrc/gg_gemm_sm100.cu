@@ -1,0 +1,241 @@
+// gg_gemm_sm100.cu — host launcher of K1 (protected GEMM) and K4 (replay).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "gg_gemm_sm100.cuh"
+#include "gg_internal.h"
+
+namespace gg {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D K-major operand [rows, K] with row pitch ld_bytes; box = (128 B of K, box_rows).
+int make_operand_map(CUtensorMap* map, CUtensorMapDataType dt, int elem, const void* ptr, int64_t K, int64_t rows,
+                     int64_t ld_bytes, uint32_t box_rows) {
+  auto enc = tensor_map_encoder();
+  if (enc == nullptr) return fail(GG_ECUDA, "cuTensorMapEncodeTiled is unavailable (driver too old?)");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_bytes)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK_BYTES / elem), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(GG_ECUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string(int(r)) + ")");
+  return 0;
+}
+
+int num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int cache[64] = {0};
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cache[dev] = n;
+  return n;
+}
+
+struct WsLayout {
+  size_t counters, band_counter, band_active, band_nflag, band_maxkey, pred, partial, total;
+};
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+WsLayout ws_layout(int64_t M, int64_t N) {
+  const size_t m_tiles = static_cast<size_t>((M + BM - 1) / BM);
+  const size_t n_tiles = static_cast<size_t>((N + BN - 1) / BN);
+  const size_t m_pad = m_tiles * BM;
+  WsLayout L{};
+  size_t off = 0;
+  L.counters = off; off = align_up(off + 16, 256);
+  L.band_counter = off; off = align_up(off + 4 * m_tiles, 256);
+  L.band_active = off; off = align_up(off + m_tiles, 256);
+  L.band_nflag = off; off = align_up(off + 4 * m_tiles, 256);
+  L.band_maxkey = off; off = align_up(off + 8 * m_tiles, 256);
+  L.pred = off; off = align_up(off + 8 * m_pad, 256);
+  L.partial = off; off = align_up(off + 8 * m_pad * n_tiles, 256);
+  L.total = off;
+  return L;
+}
+
+__global__ void replay_prepare_kernel(const uint8_t* rows, int M, int m_tiles, uint8_t* band_active, int* counters,
+                                      int* changed) {
+  // one warp per band; one block does the count
+  __shared__ int s_count;
+  if (threadIdx.x == 0) s_count = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int m = warp; m < m_tiles; m += nw) {
+    int any = 0;
+    for (int r = m * BM + lane; r < min((m + 1) * BM, M); r += 32) any |= rows[r] ? 1 : 0;
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) {
+      band_active[m] = any ? 1 : 0;
+      if (any) atomicAdd(&s_count, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    counters[0] = 0;
+    counters[1] = s_count;
+    if (changed) *changed = 0;
+  }
+}
+
+template <int KIND, int OUT, bool PROTECT>
+int launch_instance(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, cudaStream_t s) {
+  auto kern = gg_protected_gemm_kernel<KIND, OUT, PROTECT>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
+      return fail(GG_ECUDA, "cudaFuncSetAttribute(max dynamic smem) failed");
+    configured = true;
+  }
+  kern<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, p);
+  return check_launch("protected_gemm");
+}
+
+template <int KIND, int OUT>
+int dispatch_protect(bool protect, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid,
+                     cudaStream_t s) {
+  return protect ? launch_instance<KIND, OUT, true>(ta, tb, p, grid, s)
+                 : launch_instance<KIND, OUT, false>(ta, tb, p, grid, s);
+}
+
+}  // namespace
+
+size_t protected_gemm_workspace_bytes(int64_t M, int64_t N) { return ws_layout(M, N).total; }
+
+int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
+  if (d == nullptr) return fail(GG_EINVAL, "protected_gemm: null descriptor");
+  if (d->M < 1 || d->N < 1 || d->K < 1) return fail(GG_EINVAL, "gemm dims mismatch: M, N, K must be positive");
+  if (d->M > (int64_t(1) << 30) || d->N > (int64_t(1) << 30) || d->K > (int64_t(1) << 30))
+    return fail(GG_EINVAL, "protected_gemm: dims beyond 2^30");
+  int kind, elem;
+  CUtensorMapDataType tdt;
+  switch (d->ab_kind) {
+    case GG_BF16: kind = K_BF16; elem = 2; tdt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16; break;
+    case GG_F16: kind = K_F16; elem = 2; tdt = CU_TENSOR_MAP_DATA_TYPE_FLOAT16; break;
+    case GG_F32: kind = K_TF32; elem = 4; tdt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32; break;
+    case GG_I8: kind = K_I8; elem = 1; tdt = CU_TENSOR_MAP_DATA_TYPE_UINT8; break;
+    default: return fail(GG_EUNSUPPORTED, "protected_gemm: ab_kind must be GG_BF16, GG_F16, GG_F32 or GG_I8");
+  }
+  int out;
+  switch (d->c_dtype) {
+    case GG_BF16: out = O_BF16; break;
+    case GG_F16: out = O_F16; break;
+    case GG_F32: out = O_F32; break;
+    case GG_I32: out = O_I32; break;
+    default: return fail(GG_EUNSUPPORTED, "protected_gemm: unsupported c_dtype");
+  }
+  const bool int_kind = kind == K_I8;
+  if (int_kind != (out == O_I32)) return fail(GG_EINVAL, "protected_gemm: int8 operands produce int32 outputs only");
+  if (kind == K_BF16 && out == O_F16) return fail(GG_EUNSUPPORTED, "protected_gemm: bf16 -> f16 output not built");
+  if (kind == K_F16 && out == O_BF16) return fail(GG_EUNSUPPORTED, "protected_gemm: f16 -> bf16 output not built");
+  if (kind == K_TF32 && out != O_F32) return fail(GG_EUNSUPPORTED, "protected_gemm: tf32 produces f32 outputs only");
+  if ((reinterpret_cast<uintptr_t>(d->A) & 15) || (reinterpret_cast<uintptr_t>(d->B) & 15))
+    return fail(GG_EINVAL, "protected_gemm: A and B must be 16-byte aligned");
+  if ((d->lda * elem) % 16 || (d->ldb * elem) % 16)
+    return fail(GG_EINVAL, "protected_gemm: lda/ldb must be multiples of 16 bytes");
+  if (d->lda < d->K || d->ldb < d->K || d->ldc < d->N) return fail(GG_EINVAL, "protected_gemm: leading dims too small");
+  const bool protect = d->protect != 0;
+  if (protect || replay) {
+    if (int_kind && d->chk_prec != GG_P_I64)
+      return fail(GG_EINVAL, "integer layers require the int64-exact checksum precision");
+    if (!int_kind && d->chk_prec != GG_P_F64)
+      return fail(GG_EUNSUPPORTED, "fused checksum supports binary64 precision for float kinds (use gg_verify_rows)");
+    if (!d->w_sum || !d->d || !d->flags || !d->max_disc || !d->nflag || !d->triggered)
+      return fail(GG_EINVAL, "protected_gemm: protect=1 needs w_sum, d, flags, max_disc, nflag, triggered");
+    if (!d->workspace || d->workspace_bytes < protected_gemm_workspace_bytes(d->M, d->N))
+      return fail(GG_EWORKSPACE, "protected_gemm: workspace too small");
+  }
+  if (replay && !protect) return fail(GG_EINVAL, "replay_tiles: requires protect=1");
+  if (replay && d->replay_rows == nullptr) return fail(GG_EINVAL, "replay_tiles: replay_rows is NULL");
+  if (d->n_inj < 0 || (d->n_inj > 0 && d->inj == nullptr)) return fail(GG_EINVAL, "protected_gemm: bad injection list");
+
+  CUtensorMap ta, tb;
+  int rc = make_operand_map(&ta, tdt, elem, d->A, d->K, d->M, d->lda * elem, BM);
+  if (rc) return rc;
+  rc = make_operand_map(&tb, tdt, elem, d->B, d->K, d->N, d->ldb * elem, BN);
+  if (rc) return rc;
+
+  Params p{};
+  p.M = static_cast<int>(d->M);
+  p.N = static_cast<int>(d->N);
+  p.K = static_cast<int>(d->K);
+  p.m_tiles = static_cast<int>((d->M + BM - 1) / BM);
+  p.n_tiles = static_cast<int>((d->N + BN - 1) / BN);
+  p.k_blocks = static_cast<int>((d->K * elem + BK_BYTES - 1) / BK_BYTES);
+  p.m_pad = p.m_tiles * BM;
+  p.C = d->C;
+  p.ldc = d->ldc;
+  p.bias = d->bias;
+  p.chk_int = int_kind ? 1 : 0;
+  p.w_sum = d->w_sum;
+  p.bias_sum_f = d->bias_sum_f;
+  p.bias_sum_i = d->bias_sum_i;
+  p.mu = d->mu;
+  p.lo = d->lo;
+  p.hi = d->hi;
+  p.statistic = d->statistic;
+  p.d = d->d;
+  p.flags = d->flags;
+  p.max_disc = d->max_disc;
+  p.nflag = d->nflag;
+  p.triggered = d->triggered;
+  p.inj = d->inj;
+  p.n_inj = d->n_inj;
+  p.replay = replay ? 1 : 0;
+  p.changed = d->changed;
+  if (protect) {
+    const WsLayout L = ws_layout(d->M, d->N);
+    uint8_t* w = static_cast<uint8_t*>(d->workspace);
+    p.ws.counters = reinterpret_cast<int*>(w + L.counters);
+    p.ws.band_counter = reinterpret_cast<int*>(w + L.band_counter);
+    p.ws.band_active = w + L.band_active;
+    p.ws.band_nflag = reinterpret_cast<int*>(w + L.band_nflag);
+    p.ws.band_maxkey = reinterpret_cast<unsigned long long*>(w + L.band_maxkey);
+    p.ws.pred = reinterpret_cast<double*>(w + L.pred);
+    p.ws.partial = reinterpret_cast<double*>(w + L.partial);
+  }
+  if (replay) {
+    replay_prepare_kernel<<<1, 1024, 0, s>>>(d->replay_rows, p.M, p.m_tiles, p.ws.band_active, p.ws.counters,
+                                              d->changed);
+    rc = check_launch("replay_prepare");
+    if (rc) return rc;
+  }
+  const int tiles = p.m_tiles * p.n_tiles;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+
+  switch (kind) {
+    case K_BF16:
+      return out == O_BF16 ? dispatch_protect<K_BF16, O_BF16>(protect, ta, tb, p, grid, s)
+                           : dispatch_protect<K_BF16, O_F32>(protect, ta, tb, p, grid, s);
+    case K_F16:
+      return out == O_F16 ? dispatch_protect<K_F16, O_F16>(protect, ta, tb, p, grid, s)
+                          : dispatch_protect<K_F16, O_F32>(protect, ta, tb, p, grid, s);
+    case K_TF32:
+      return dispatch_protect<K_TF32, O_F32>(protect, ta, tb, p, grid, s);
+    default:
+      return dispatch_protect<K_I8, O_I32>(protect, ta, tb, p, grid, s);
+  }
+}
+
+}  // namespace gg

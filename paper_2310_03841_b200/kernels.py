@@ -1,0 +1,386 @@
+"""Torch-tensor front end of the C-ABI kernels (device memory in, device memory out).
+
+torch is plumbing here: it owns device memory and the current stream; every
+computation runs in ``libgemmguard_b200.so``.  Functions raise ValueError for
+bad shapes/dtypes (the reference's convention) and never fall back to a CPU
+path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+TORCH_TO_GG = {
+    torch.float64: L.GG_F64,
+    torch.float32: L.GG_F32,
+    torch.float16: L.GG_F16,
+    torch.bfloat16: L.GG_BF16,
+    torch.int8: L.GG_I8,
+    torch.int32: L.GG_I32,
+    torch.int64: L.GG_I64,
+}
+PREC_TORCH = {
+    L.GG_P_F16: torch.float16,
+    L.GG_P_F32: torch.float32,
+    L.GG_P_F64: torch.float64,
+    L.GG_P_I64: torch.int64,
+}
+
+INJ_DTYPE = np.dtype(
+    [("row", "<i8"), ("col", "<i4"), ("bit", "<i4"), ("target", "<i4"), ("mode", "<i4"), ("value", "<f8")]
+)
+assert INJ_DTYPE.itemsize == ctypes.sizeof(L.GGInjection)
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _require_cuda(*ts: torch.Tensor | None) -> torch.device:
+    dev = None
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("device kernels take CUDA tensors (no CPU fallback)")
+        dev = t.device if dev is None else dev
+    if dev is None:
+        raise ValueError("no CUDA tensor given")
+    return dev
+
+
+@dataclass
+class Injection:
+    """One fault for the protected-GEMM epilogue (gg_injection)."""
+
+    row: int
+    col: int
+    bit: int = 0
+    target: int = L.GG_INJ_OUTPUT
+    mode: int = L.GG_INJ_BITFLIP
+    value: float = 0.0
+
+
+def injections_to_device(injs: Sequence[Injection], device: torch.device) -> torch.Tensor:
+    arr = np.zeros(len(injs), dtype=INJ_DTYPE)
+    for i, f in enumerate(injs):
+        arr[i] = (f.row, f.col, f.bit, f.target, f.mode, f.value)
+    return torch.from_numpy(arr.view(np.uint8).copy()).to(device, non_blocking=False)
+
+
+@dataclass
+class CheckResult:
+    """Device-resident outcome of one protected launch (guard.DetectionOutcome)."""
+
+    d: torch.Tensor  # [M] f64 or i64
+    flags: torch.Tensor  # [M] u8
+    max_disc: torch.Tensor  # [1] f64
+    nflag: torch.Tensor  # [1] i32
+    triggered: torch.Tensor  # [1] u8
+
+    @classmethod
+    def empty(cls, M: int, integer: bool, device) -> "CheckResult":
+        return cls(
+            d=torch.empty(M, dtype=torch.int64 if integer else torch.float64, device=device),
+            flags=torch.empty(M, dtype=torch.uint8, device=device),
+            max_disc=torch.empty(1, dtype=torch.float64, device=device),
+            nflag=torch.empty(1, dtype=torch.int32, device=device),
+            triggered=torch.empty(1, dtype=torch.uint8, device=device),
+        )
+
+
+_WS: dict[tuple, torch.Tensor] = {}
+
+
+def workspace(M: int, N: int, device: torch.device, key=None) -> torch.Tensor:
+    """Zero-initialised workspace for (M, N); every launch leaves it re-zeroed."""
+    nbytes = int(L.load().gg_protected_gemm_workspace_bytes(M, N))
+    k = (device, M, N, key)
+    ws = _WS.get(k)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        _WS[k] = ws
+    return ws
+
+
+def _pad_k(t: torch.Tensor) -> torch.Tensor:
+    """Row pitch must be a multiple of 16 bytes for TMA: pad storage, keep K."""
+    K = t.shape[1]
+    es = t.element_size()
+    if t.stride(1) == 1 and (t.stride(0) * es) % 16 == 0 and t.data_ptr() % 16 == 0 and t.stride(0) >= K:
+        return t
+    step = 16 // es
+    Kp = (K + step - 1) // step * step
+    buf = torch.zeros((t.shape[0], Kp), dtype=t.dtype, device=t.device)
+    buf[:, :K] = t
+    return buf[:, :K]
+
+
+def build_desc(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    y: torch.Tensor,
+    bias: torch.Tensor | None,
+    *,
+    protect: bool,
+    w_sum: torch.Tensor | None = None,
+    bias_sum: float | int = 0,
+    mu: float = 0.0,
+    lo: float = 0.0,
+    hi: float = 0.0,
+    statistic: int = L.GG_PER_SAMPLE,
+    result: CheckResult | None = None,
+    inj_dev: torch.Tensor | None = None,
+    n_inj: int = 0,
+    ws: torch.Tensor | None = None,
+    replay_rows: torch.Tensor | None = None,
+    changed: torch.Tensor | None = None,
+) -> L.GGGemmDesc:
+    M, K = x.shape
+    N = w.shape[0]
+    d = L.GGGemmDesc()
+    d.ab_kind = TORCH_TO_GG[x.dtype]
+    d.c_dtype = TORCH_TO_GG[y.dtype]
+    d.M, d.N, d.K = M, N, K
+    d.A, d.lda = x.data_ptr(), x.stride(0)
+    d.B, d.ldb = w.data_ptr(), w.stride(0)
+    d.bias = _ptr(bias)
+    d.C, d.ldc = y.data_ptr(), y.stride(0)
+    d.protect = 1 if protect else 0
+    integer = x.dtype == torch.int8
+    d.chk_prec = L.GG_P_I64 if integer else L.GG_P_F64
+    if protect:
+        d.w_sum = _ptr(w_sum)
+        if integer:
+            d.bias_sum_i = int(bias_sum)
+        else:
+            d.bias_sum_f = float(bias_sum)
+        d.mu, d.lo, d.hi, d.statistic = float(mu), float(lo), float(hi), int(statistic)
+        d.d = result.d.data_ptr()
+        d.flags = result.flags.data_ptr()
+        d.max_disc = result.max_disc.data_ptr()
+        d.nflag = result.nflag.data_ptr()
+        d.triggered = result.triggered.data_ptr()
+        d.workspace = ws.data_ptr()
+        d.workspace_bytes = ws.numel()
+    d.inj = _ptr(inj_dev)
+    d.n_inj = int(n_inj)
+    d.replay_rows = _ptr(replay_rows)
+    d.changed = _ptr(changed)
+    return d
+
+
+def _check_gemm_operands(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None):
+    if x.dim() != 2 or w.dim() != 2:
+        raise ValueError("protected_gemm requires 2-D operands")
+    if x.shape[1] != w.shape[1]:
+        raise ValueError(f"gemm dims mismatch: X is {tuple(x.shape)}, W is {tuple(w.shape)} ([N, K])")
+    if x.dtype != w.dtype:
+        raise ValueError(f"gemm operand dtypes differ: {x.dtype} vs {w.dtype}")
+    if x.dtype not in (torch.bfloat16, torch.float16, torch.float32, torch.int8):
+        raise ValueError(f"tensor-core path takes bf16, fp16, fp32 (tf32) or int8 operands, got {x.dtype}")
+    if bias is not None:
+        want = torch.int32 if x.dtype == torch.int8 else torch.float32
+        if bias.dtype != want or bias.dim() != 1 or bias.shape[0] != w.shape[0]:
+            raise ValueError(f"bias must be a [{w.shape[0]}] {want} tensor")
+
+
+def default_out_dtype(ab: torch.dtype) -> torch.dtype:
+    """Result rounded to the operand dtype (numerics.py:289); int8 -> int32."""
+    return {torch.bfloat16: torch.bfloat16, torch.float16: torch.float16, torch.float32: torch.float32,
+            torch.int8: torch.int32}[ab]
+
+
+def protected_gemm(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    bias: torch.Tensor | None = None,
+    *,
+    out_dtype: torch.dtype | None = None,
+    protect: bool = True,
+    w_sum: torch.Tensor | None = None,
+    bias_sum: float | int = 0,
+    mu: float = 0.0,
+    lo: float = 0.0,
+    hi: float = 0.0,
+    statistic: int = L.GG_PER_SAMPLE,
+    injections: Sequence[Injection] | torch.Tensor | None = None,
+    out: torch.Tensor | None = None,
+    result: CheckResult | None = None,
+    ws_key=None,
+) -> tuple[torch.Tensor, CheckResult | None]:
+    """K1: y = x @ w.T + bias with the fused checksum check (one launch).
+
+    x [M, K], w [N, K] (torch Linear layout), bias [N] (f32, or i32 for int8).
+    Returns (y, CheckResult or None when protect=False).
+    """
+    dev = _require_cuda(x, w, bias)
+    _check_gemm_operands(x, w, bias)
+    x = _pad_k(x)
+    w = _pad_k(w)
+    M, N = x.shape[0], w.shape[0]
+    odt = out_dtype or default_out_dtype(x.dtype)
+    y = out if out is not None else torch.empty((M, N), dtype=odt, device=dev)
+    if protect:
+        if w_sum is None:
+            raise ValueError("protect=True needs the offline checksum w_sum")
+        result = result or CheckResult.empty(M, x.dtype == torch.int8, dev)
+        ws = workspace(M, N, dev, ws_key)
+    else:
+        ws = None
+    if isinstance(injections, torch.Tensor):
+        inj_dev, n_inj = injections, injections.numel() // INJ_DTYPE.itemsize
+    elif injections:
+        inj_dev, n_inj = injections_to_device(injections, dev), len(injections)
+    else:
+        inj_dev, n_inj = None, 0
+    desc = build_desc(x, w, y, bias, protect=protect, w_sum=w_sum, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
+                      statistic=statistic, result=result, inj_dev=inj_dev, n_inj=n_inj, ws=ws)
+    L.check(L.load().gg_protected_gemm(ctypes.byref(desc), _stream(dev)), "gg_protected_gemm")
+    return y, (result if protect else None)
+
+
+def replay_tiles(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    bias: torch.Tensor | None,
+    y: torch.Tensor,
+    replay_rows: torch.Tensor,
+    result: CheckResult,
+    *,
+    w_sum: torch.Tensor,
+    bias_sum: float | int = 0,
+    mu: float = 0.0,
+    lo: float = 0.0,
+    hi: float = 0.0,
+    statistic: int = L.GG_PER_SAMPLE,
+    changed: torch.Tensor | None = None,
+    ws_key=None,
+) -> torch.Tensor:
+    """K4: recompute only the M-bands holding a flagged row, in place in y.
+
+    Returns the device scalar count of outputs whose bytes changed (0 means
+    the recompute reproduced the flagged output: guard.py:590-594).
+    """
+    dev = _require_cuda(x, w, y, replay_rows)
+    _check_gemm_operands(x, w, bias)
+    x = _pad_k(x)
+    w = _pad_k(w)
+    M, N = x.shape[0], w.shape[0]
+    changed = changed if changed is not None else torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = workspace(M, N, dev, ws_key)
+    desc = build_desc(x, w, y, bias, protect=True, w_sum=w_sum, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
+                      statistic=statistic, result=result, ws=ws, replay_rows=replay_rows, changed=changed)
+    L.check(L.load().gg_replay_tiles(ctypes.byref(desc), _stream(dev)), "gg_replay_tiles")
+    return changed
+
+
+def offline_checksum(
+    w: torch.Tensor, bias: torch.Tensor | None, prec: int, *, layout: int = 0
+) -> tuple[torch.Tensor, torch.Tensor]:
+    """K2: (w_sum [K], bias_sum [1]) in precision `prec` (bit-exact, guard.py:142-160).
+
+    layout 0: w is [N, K] (torch); layout 1: w is Wt [K, N] (reference)."""
+    dev = _require_cuda(w, bias)
+    w = w.contiguous()
+    if layout == 0:
+        N, K = w.shape
+    else:
+        K, N = w.shape
+    pt = PREC_TORCH[prec]
+    w_sum = torch.empty(K, dtype=pt, device=dev)
+    bsum = torch.empty(1, dtype=pt, device=dev)
+    b = None if bias is None else bias.contiguous()
+    L.check(
+        L.load().gg_offline_checksum(
+            TORCH_TO_GG[w.dtype], w.data_ptr(), K, N, w.stride(0), layout, _ptr(b),
+            TORCH_TO_GG[b.dtype] if b is not None else 0, prec, w_sum.data_ptr(), bsum.data_ptr(), _stream(dev),
+        ),
+        "gg_offline_checksum",
+    )
+    return w_sum, bsum
+
+
+def verify_rows(
+    x: torch.Tensor,
+    y: torch.Tensor,
+    w_sum: torch.Tensor,
+    bias_sum: torch.Tensor,
+    prec: int,
+    *,
+    mu: float = 0.0,
+    lo: float = 0.0,
+    hi: float = 0.0,
+    statistic: int = L.GG_PER_SAMPLE,
+) -> CheckResult:
+    """Reference-exact guard._discrepancies + _verify_arrays on a given (X, Y)."""
+    dev = _require_cuda(x, y, w_sum, bias_sum)
+    x = x.contiguous()
+    y = y.contiguous()
+    M, K = x.shape
+    N = y.shape[1]
+    res = CheckResult.empty(M, prec == L.GG_P_I64, dev)
+    L.check(
+        L.load().gg_verify_rows(
+            TORCH_TO_GG[x.dtype], x.data_ptr(), M, K, x.stride(0), TORCH_TO_GG[y.dtype], y.data_ptr(), N,
+            y.stride(0), prec, w_sum.data_ptr(), bias_sum.data_ptr(), float(mu), float(lo), float(hi),
+            int(statistic), res.d.data_ptr(), res.flags.data_ptr(), res.max_disc.data_ptr(),
+            res.nflag.data_ptr(), res.triggered.data_ptr(), _stream(dev),
+        ),
+        "gg_verify_rows",
+    )
+    return res
+
+
+def flip_bits(buf: torch.Tensor, elem_idx: torch.Tensor, bit_idx: torch.Tensor) -> None:
+    """K3: in-place XOR of bit bit_idx[i] of element elem_idx[i] (involution)."""
+    dev = _require_cuda(buf, elem_idx, bit_idx)
+    if elem_idx.dtype != torch.int64 or bit_idx.dtype != torch.int32:
+        raise ValueError("flip_bits: elem_idx must be int64 and bit_idx int32")
+    n = elem_idx.numel()
+    L.check(
+        L.load().gg_flip_bits(buf.data_ptr(), buf.element_size(), elem_idx.data_ptr(), bit_idx.data_ptr(), n,
+                              _stream(dev)),
+        "gg_flip_bits",
+    )
+
+
+def gemm_exact(x: torch.Tensor, wt: torch.Tensor, bias: torch.Tensor | None, accum: int) -> torch.Tensor:
+    """Bit-exact numerics.gemm on CUDA cores: x [M,K], wt [K,N] (reference layout)."""
+    dev = _require_cuda(x, wt, bias)
+    x = x.contiguous()
+    wt = wt.contiguous()
+    M, K = x.shape
+    N = wt.shape[1]
+    odt = torch.int32 if x.dtype == torch.int8 else x.dtype
+    y = torch.empty((M, N), dtype=odt, device=dev)
+    b = None if bias is None else bias.contiguous()
+    L.check(
+        L.load().gg_gemm_exact(TORCH_TO_GG[x.dtype], accum, x.data_ptr(), M, K, wt.data_ptr(), N, _ptr(b),
+                               y.data_ptr(), _stream(dev)),
+        "gg_gemm_exact",
+    )
+    return y
+
+
+def reduce(a: torch.Tensor, axis: int) -> torch.Tensor:
+    """numerics.reduce_rows (axis=1) / reduce_cols (axis=0), ascending folds."""
+    dev = _require_cuda(a)
+    a = a.contiguous()
+    rows, cols = a.shape
+    integer = a.dtype in (torch.int8, torch.int32, torch.int64)
+    out = torch.empty(rows if axis == 1 else cols, dtype=torch.int64 if integer else torch.float64, device=dev)
+    L.check(L.load().gg_reduce(TORCH_TO_GG[a.dtype], a.data_ptr(), rows, cols, axis, out.data_ptr(), _stream(dev)),
+            "gg_reduce")
+    return out
