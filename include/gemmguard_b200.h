@@ -100,6 +100,7 @@ typedef struct gg_gemm_desc {
   int32_t protect;            /* 0: unprotected baseline of the same kernel  */
   int32_t chk_prec;           /* GG_P_F64 (float kinds) or GG_P_I64 (GG_I8)  */
   const void* w_sum;          /* [K] f64 or i64: gg_offline_checksum output  */
+  const void* w_aux;          /* gg_checksum_aux output for this ab_kind     */
   double bias_sum_f;          /* bias_sum for GG_P_F64                       */
   int64_t bias_sum_i;         /* bias_sum for GG_P_I64                       */
   double mu, lo, hi;          /* EpsilonModel mu, threshold_low/high         */
@@ -152,6 +153,19 @@ GG_API int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_
                         int64_t ldw, int32_t w_layout, const void* bias,
                         int32_t bias_dtype, int32_t chk_prec, void* w_sum_out,
                         void* bias_sum_out, void* stream);
+
+/* Side-path encoding of w_sum consumed by the fused checksum of K1, computed
+ * once per weight (offline, like w_sum itself):
+ *   GG_BF16 / GG_F16: float2 [K] = (hi, lo) with hi = fp32(w_sum),
+ *                     lo = fp32(w_sum - hi), so x*w_sum is formed with fp32
+ *                     FMAs and folded into fp64 every 16 products;
+ *   GG_I8:            int32x4 [ceil(K/4)] signed base-256 digit planes of the
+ *                     int64 w_sum (|w_sum| < 2^23), so x*w_sum is an exact
+ *                     IDP4A dot product;
+ *   GG_F32:           none (0 bytes; the tf32 path reads w_sum directly). */
+GG_API size_t gg_checksum_aux_bytes(int32_t ab_kind, int64_t K);
+GG_API int gg_checksum_aux(int32_t ab_kind, const void* w_sum, int64_t K, void* aux_out,
+                           void* stream);
 
 /* Reference-exact verification of a given (X, Y): sequential folds in the
  * checksum precision exactly as guard._discrepancies (guard.py:163-171) and

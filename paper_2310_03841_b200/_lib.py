@@ -30,6 +30,8 @@ EXPORTED_SYMBOLS = (
     "gg_protected_gemm_workspace_bytes",
     "gg_protected_gemm",
     "gg_replay_tiles",
+    "gg_checksum_aux_bytes",
+    "gg_checksum_aux",
     "gg_offline_checksum",
     "gg_verify_rows",
     "gg_flip_bits",
@@ -67,6 +69,7 @@ class GGGemmDesc(ctypes.Structure):
         ("protect", c_int32),
         ("chk_prec", c_int32),
         ("w_sum", c_void_p),
+        ("w_aux", c_void_p),
         ("bias_sum_f", c_double),
         ("bias_sum_i", c_int64),
         ("mu", c_double),
@@ -118,6 +121,10 @@ def load(path: Path | None = None):
     lib.gg_protected_gemm.argtypes = [POINTER(GGGemmDesc), c_void_p]
     lib.gg_replay_tiles.restype = c_int32
     lib.gg_replay_tiles.argtypes = [POINTER(GGGemmDesc), c_void_p]
+    lib.gg_checksum_aux_bytes.restype = c_size_t
+    lib.gg_checksum_aux_bytes.argtypes = [c_int32, c_int64]
+    lib.gg_checksum_aux.restype = c_int32
+    lib.gg_checksum_aux.argtypes = [c_int32, c_void_p, c_int64, c_void_p, c_void_p]
     lib.gg_offline_checksum.restype = c_int32
     lib.gg_offline_checksum.argtypes = [
         c_int32, c_void_p, c_int64, c_int64, c_int64, c_int32, c_void_p, c_int32, c_int32, c_void_p, c_void_p,

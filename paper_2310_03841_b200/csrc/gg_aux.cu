@@ -379,6 +379,31 @@ __global__ void round_kernel(int dtype, const double* in, void* out, int64_t n) 
   else static_cast<double*>(out)[i] = v;
 }
 
+// w_sum side-path encodings for the fused checksum (see gg_checksum_aux).
+__global__ void split_f64_kernel(const double* w, int64_t K, float2* out) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= K) return;
+  const double v = w[k];
+  const float hi = __double2float_rn(v);
+  const float lo = __double2float_rn(v - static_cast<double>(hi));
+  out[k] = make_float2(hi, lo);
+}
+__global__ void digits_i64_kernel(const long long* w, int64_t K, int4* out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // group of 4 k
+  if (i * 4 >= K) return;
+  uint32_t plane[3] = {0u, 0u, 0u};
+  for (int e = 0; e < 4; ++e) {
+    const int64_t k = i * 4 + e;
+    long long v = k < K ? w[k] : 0;
+    for (int d = 0; d < 3; ++d) {
+      const long long dig = ((v + 128) & 255) - 128;  // signed digit in [-128, 127]
+      plane[d] |= (static_cast<uint32_t>(dig) & 0xFFu) << (8 * e);
+      v = (v - dig) / 256;
+    }
+  }
+  out[i] = make_int4(static_cast<int>(plane[0]), static_cast<int>(plane[1]), static_cast<int>(plane[2]), 0);
+}
+
 inline unsigned grid1(int64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
 }  // namespace
@@ -482,6 +507,33 @@ int launch_gemm_exact(int dtype, int accum, const void* X, int64_t M, int64_t K,
   else
     gemm_exact_kernel<AccF32, 0><<<grid, 128, 0, s>>>(dtype, X, M, K, Wt, N, bias, Y, start_zero);
   return check_launch("gemm_exact");
+}
+
+size_t checksum_aux_bytes(int ab_kind, int64_t K) {
+  if (K < 1) return 0;
+  switch (ab_kind) {
+    case GG_BF16: case GG_F16: return static_cast<size_t>(K) * 8;
+    case GG_I8: return static_cast<size_t>((K + 3) / 4) * 16;
+    default: return 0;
+  }
+}
+
+int launch_checksum_aux(int ab_kind, const void* w_sum, int64_t K, void* aux, cudaStream_t s) {
+  if (K < 1) return fail(GG_EINVAL, "checksum_aux: empty w_sum");
+  switch (ab_kind) {
+    case GG_BF16: case GG_F16:
+      split_f64_kernel<<<grid1(K, 256), 256, 0, s>>>(static_cast<const double*>(w_sum), K, static_cast<float2*>(aux));
+      break;
+    case GG_I8:
+      digits_i64_kernel<<<grid1((K + 3) / 4, 256), 256, 0, s>>>(static_cast<const long long*>(w_sum), K,
+                                                              static_cast<int4*>(aux));
+      break;
+    case GG_F32:
+      return 0;
+    default:
+      return fail(GG_EINVAL, "checksum_aux: unknown ab_kind");
+  }
+  return check_launch("checksum_aux");
 }
 
 int launch_reduce(int dtype, const void* A, int64_t rows, int64_t cols, int axis, void* out, cudaStream_t s) {

@@ -44,6 +44,12 @@ int gg_replay_tiles(const gg_gemm_desc* desc, void* stream) {
   return gg::launch_protected_gemm(desc, true, static_cast<cudaStream_t>(stream));
 }
 
+size_t gg_checksum_aux_bytes(int32_t ab_kind, int64_t K) { return gg::checksum_aux_bytes(ab_kind, K); }
+
+int gg_checksum_aux(int32_t ab_kind, const void* w_sum, int64_t K, void* aux_out, void* stream) {
+  return gg::launch_checksum_aux(ab_kind, w_sum, K, aux_out, static_cast<cudaStream_t>(stream));
+}
+
 int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_t N, int64_t ldw, int32_t w_layout,
                         const void* bias, int32_t bias_dtype, int32_t chk_prec, void* w_sum_out,
                         void* bias_sum_out, void* stream) {

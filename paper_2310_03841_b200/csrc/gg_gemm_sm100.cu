@@ -69,7 +69,7 @@ WsLayout ws_layout(int64_t M, int64_t N) {
   L.band_active = off; off = align_up(off + m_tiles, 256);
   L.band_nflag = off; off = align_up(off + 4 * m_tiles, 256);
   L.band_maxkey = off; off = align_up(off + 8 * m_tiles, 256);
-  L.pred = off; off = align_up(off + 8 * m_pad, 256);
+  L.pred = off; off = align_up(off + 8 * m_pad * n_tiles, 256);
   L.partial = off; off = align_up(off + 8 * m_pad * n_tiles, 256);
   L.total = off;
   return L;
@@ -161,12 +161,20 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
       return fail(GG_EINVAL, "integer layers require the int64-exact checksum precision");
     if (!int_kind && d->chk_prec != GG_P_F64)
       return fail(GG_EUNSUPPORTED, "fused checksum supports binary64 precision for float kinds (use gg_verify_rows)");
+    if (reinterpret_cast<uintptr_t>(d->w_sum) & 15) return fail(GG_EINVAL, "protected_gemm: w_sum must be 16-byte aligned");
+    if ((kind == K_BF16 || kind == K_F16 || kind == K_I8) &&
+        (d->w_aux == nullptr || (reinterpret_cast<uintptr_t>(d->w_aux) & 15)))
+      return fail(GG_EINVAL, "protected_gemm: w_aux (gg_checksum_aux) is required and must be 16-byte aligned");
     if (!d->w_sum || !d->d || !d->flags || !d->max_disc || !d->nflag || !d->triggered)
       return fail(GG_EINVAL, "protected_gemm: protect=1 needs w_sum, d, flags, max_disc, nflag, triggered");
     if (!d->workspace || d->workspace_bytes < protected_gemm_workspace_bytes(d->M, d->N))
       return fail(GG_EWORKSPACE, "protected_gemm: workspace too small");
   }
   if (replay && !protect) return fail(GG_EINVAL, "replay_tiles: requires protect=1");
+  if (int_kind && protect && d->N > 65535)
+    return fail(GG_EUNSUPPORTED, "protected_gemm: int8 checksum path supports N <= 65535 (|w_sum| < 2^23)");
+  if (int_kind && protect && d->K > (int64_t(1) << 17))
+    return fail(GG_EUNSUPPORTED, "protected_gemm: int8 checksum path supports K <= 131072");
   if (replay && d->replay_rows == nullptr) return fail(GG_EINVAL, "replay_tiles: replay_rows is NULL");
   if (d->n_inj < 0 || (d->n_inj > 0 && d->inj == nullptr)) return fail(GG_EINVAL, "protected_gemm: bad injection list");
 
@@ -187,8 +195,8 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.C = d->C;
   p.ldc = d->ldc;
   p.bias = d->bias;
-  p.chk_int = int_kind ? 1 : 0;
   p.w_sum = d->w_sum;
+  p.w_aux = d->w_aux;
   p.bias_sum_f = d->bias_sum_f;
   p.bias_sum_i = d->bias_sum_i;
   p.mu = d->mu;

@@ -13,12 +13,13 @@
 //   warps 4-7   epilogue: tcgen05.ld one accumulator row per thread, bias,
 //               round to the output type, fault injection, store, and the
 //               OBSERVED row sum over the stored values (guard.py:170)
-//   warps 8-11  checksum producer side: on the first N-tile of every M-band,
-//               read the A stages from shared memory as they stream past the
-//               MMA and form PREDICTED[m] = A[m,:] . w_sum (guard.py:168-169)
-//               in fp64 — no extra pass over X in HBM.
-// Per M-band, the last of the (n_tiles + 1) contributions folds the per-tile
-// observed partials in ascending tile order, forms d, flags and per-band
+//   warps 8-11  checksum producer side: read the A stages from shared memory
+//               as they stream past the MMA and form PREDICTED[m] =
+//               A[m,:] . w_sum (guard.py:168-169) in fp64 (int64 for int8) —
+//               no extra pass over X in HBM; K-blocks are dealt round-robin
+//               over the band's N-tiles.
+// Per M-band, the last of the 2*n_tiles contributions folds the per-tile
+// observed and predicted partials in ascending tile order, forms d, flags and per-band
 // summaries; the last band forms the launch summaries (nflag, triggered,
 // max_disc) and resets the counters.  Everything is deterministic: no atomics
 // touch C or d, so a recompute is byte-identical (needed by replay,
@@ -53,8 +54,8 @@ struct Workspace {
   uint8_t* band_active; // [m_tiles]
   int* band_nflag;      // [m_tiles]
   unsigned long long* band_maxkey;  // [m_tiles]
-  double* pred;         // [m_pad]
-  double* partial;      // [n_tiles * m_pad]
+  double* pred;         // [n_tiles * m_pad] predicted partials (i64 bits for int)
+  double* partial;      // [n_tiles * m_pad] observed partials (i64 bits for int)
 };
 
 struct Params {
@@ -64,8 +65,8 @@ struct Params {
   long long ldc;
   const void* bias;
   // checksum
-  int chk_int;          // 1: int64 semantics
   const void* w_sum;    // f64 or i64
+  const void* w_aux;    // bf16/f16: float2 (hi, lo) split of w_sum; i8: int32x4 signed digit planes
   double bias_sum_f;
   long long bias_sum_i;
   double mu, lo, hi;
@@ -168,56 +169,71 @@ struct GroupScratch {
 // Called by a 128-thread group (epilogue or checksum side) after it has
 // published its contribution to band m.  The last contributor finalises the
 // band; the last band finalises the launch.
+template <bool INT>
 __device__ void band_arrive(const Params& p, int m, int tid, uint32_t bar, GroupScratch* gs) {
+  // Release: every thread fences its own partial write (a fence orders only
+  // the calling thread's writes), then thread 0 counts the contribution.
   __threadfence();
   named_bar_sync(bar, 128);
   if (tid == 0) {
-    int old = atomicAdd(&p.ws.band_counter[m], 1);
-    gs->flag = (old == p.n_tiles) ? 1 : 0;  // n_tiles epilogue tiles + 1 predicted
+    const int old = atomicAdd(&p.ws.band_counter[m], 1);
+    gs->flag = (old == 2 * p.n_tiles - 1) ? 1 : 0;  // n_tiles observed + n_tiles predicted partials
+    if (gs->flag) __threadfence();                  // acquire the other contributions
   }
   named_bar_sync(bar, 128);
   if (!gs->flag) return;
-  __threadfence();
 
-  // ---- finalise band m: d, flags, band summaries
+  // ---- finalise band m: d, flags, band summaries (fixed ascending tile order)
   const int row = m * BM + tid;
   int nflag = 0;
   unsigned long long key = 0;
   if (row < p.M) {
-    double obs = 0.0;
-    for (int t = 0; t < p.n_tiles; ++t) obs += ldcg_f64(&p.ws.partial[(size_t)t * p.m_pad + row]);
-    const double pred = ldcg_f64(&p.ws.pred[row]);
     bool flag;
-    if (p.chk_int) {
-      const long long di = (__double2ll_rn(pred) + p.bias_sum_i) - __double2ll_rn(obs);
+    if constexpr (INT) {
+      long long obs = 0, pred = 0;
+      const long long* part = reinterpret_cast<const long long*>(p.ws.partial);
+      const long long* predp = reinterpret_cast<const long long*>(p.ws.pred);
+      for (int t = 0; t < p.n_tiles; ++t) {
+        obs += __ldcg(&part[(size_t)t * p.m_pad + row]);
+        pred += __ldcg(&predp[(size_t)t * p.m_pad + row]);
+      }
+      const long long di = (pred + p.bias_sum_i) - obs;
       static_cast<long long*>(p.d)[row] = di;
       flag = di != 0;
-      key = gap_key(fabs(static_cast<double>(di)));
+      const unsigned long long mag = di < 0 ? 0ull - static_cast<unsigned long long>(di) : static_cast<unsigned long long>(di);
+      key = gap_key(static_cast<double>(mag));
     } else {
+      double obs = 0.0, pred = 0.0;
+      for (int t = 0; t < p.n_tiles; ++t) {
+        obs += ldcg_f64(&p.ws.partial[(size_t)t * p.m_pad + row]);
+        pred += ldcg_f64(&p.ws.pred[(size_t)t * p.m_pad + row]);
+      }
       const double dd = (pred + p.bias_sum_f) - obs;
       static_cast<double*>(p.d)[row] = dd;
       flag = !((dd >= p.lo) && (dd <= p.hi));
       key = gap_key(fabs(dd - p.mu));
     }
-    if (p.statistic == GG_PER_SAMPLE || p.chk_int) {
+    if (INT || p.statistic == GG_PER_SAMPLE) {
       p.flags[row] = flag ? 1 : 0;
       nflag = flag ? 1 : 0;
     }
   }
   nflag = group_sum_i32(nflag, tid, bar, gs->isum);
   key = group_max_u64(key, tid, bar, gs->umax);
+  __threadfence();  // d / flags of this band, before the launch-level count
+  named_bar_sync(bar, 128);
   if (tid == 0) {
     p.ws.band_nflag[m] = nflag;
     p.ws.band_maxkey[m] = key;
     p.ws.band_counter[m] = 0;
     __threadfence();
-    int total = p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles;
-    int old = atomicAdd(&p.ws.counters[0], 1);
+    const int total = p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles;
+    const int old = atomicAdd(&p.ws.counters[0], 1);
     gs->flag = (old == total - 1) ? 1 : 0;
+    if (gs->flag) __threadfence();
   }
   named_bar_sync(bar, 128);
   if (!gs->flag) return;
-  __threadfence();
 
   // ---- last band: launch summaries over ALL bands (replayed or not)
   int nf = 0;
@@ -229,7 +245,7 @@ __device__ void band_arrive(const Params& p, int m, int tid, uint32_t bar, Group
   }
   nf = group_sum_i32(nf, tid, bar, gs->isum);
   mk = group_max_u64(mk, tid, bar, gs->umax);
-  if (p.statistic == GG_BATCH_MEAN && !p.chk_int) {
+  if (!INT && p.statistic == GG_BATCH_MEAN) {
     // mean(d) over all rows in a fixed order; every row flags iff outside
     double s = 0.0;
     for (int r = tid; r < p.M; r += 128) s += ldcg_f64(&static_cast<double*>(p.d)[r]);
@@ -317,14 +333,31 @@ __device__ __forceinline__ uint32_t out_bits_mask() {
 }
 
 // ======================================================================
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// Tile t -> (m, n), N-tile fastest: the n_tiles tiles of one M-band run on
+// neighbouring CTAs at the same time, so each A band is read from HBM once
+// and B (the weight) stays L2-resident.
+__device__ __forceinline__ void tile_coords(const Params& p, int t, int& m, int& n) {
+  m = t / p.n_tiles;
+  n = t - m * p.n_tiles;
+}
+
 template <int KIND, int OUT, bool PROTECT>
 __global__ void __launch_bounds__(THREADS, 1)
     gg_protected_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const Params p) {
   using T = KindTraits<KIND>;
+  constexpr bool INT = (KIND == K_I8);
   constexpr int BK = BK_BYTES / T::ELEM;            // elements of K per stage
   constexpr int MMA_K_BYTES = 32;                   // K bytes per tcgen05.mma
   constexpr int MMAS_PER_STAGE = BK_BYTES / MMA_K_BYTES;
+  constexpr int OUT_BYTES = (OUT == O_BF16 || OUT == O_F16) ? 2 : 4;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -372,7 +405,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m = t % p.m_tiles, n = t / p.m_tiles;
+        int m, n;
+        tile_coords(p, t, m, n);
         if (!tile_active(m)) continue;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -390,7 +424,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int local = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m = t % p.m_tiles;
+        int m, n;
+        tile_coords(p, t, m, n);
         if (!tile_active(m)) continue;
         const int buf = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -420,9 +455,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ================================================= epilogue
     const int eg = warp - 4;           // TMEM lane group == warp % 4
     const int tid = threadIdx.x - 128; // 0..127 == accumulator row in tile
+    const bool vec_ok = ((p.ldc * OUT_BYTES) % 16 == 0) && ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0);
+    const bool bias_vec = (p.bias != nullptr) && ((p.N & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.bias) & 15) == 0);
     int local = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int m = t % p.m_tiles, n = t / p.m_tiles;
+      int m, n;
+      tile_coords(p, t, m, n);
       if (!tile_active(m)) continue;
       const int buf = local & 1;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -431,17 +469,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row = m * BM + tid;
       const bool row_ok = row < p.M;
       const int n0 = n * BN;
-      double obs = 0.0;
+      const int nchunks = min(BN / 32, (p.N - n0 + 31) / 32);  // chunks holding valid columns
+      double obs = 0.0;      // float kinds
+      long long obs_i = 0;   // int kind (exact)
       int changed = 0;
-      const bool vec_ok = ((p.ldc * (OUT <= O_F16 ? 2 : 4)) % 16 == 0);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < nchunks; ++c) {
         const int col0 = n0 + 32 * c;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(eg * 32) << 16) + static_cast<uint32_t>(buf * BN + 32 * c), r);
         tmem_ld_wait();
-        if (col0 >= p.N) continue;  // warp-uniform
-        // faults on this row inside this chunk (rare; list is short)
+        if (c == nchunks - 1) {
+          // all TMEM reads of this buffer are done: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+        }
+        const bool full = (col0 + 32 <= p.N);
+        // faults on this row inside this chunk (rare; the list is short)
         for (int i = 0; i < p.n_inj; ++i) {
           const gg_injection f = p.inj[i];
           if (f.row == row && f.target == GG_INJ_ACCUMULATOR && f.col >= col0 && f.col < col0 + 32) {
@@ -451,11 +496,23 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
         uint32_t o[32];
+        if (full && bias_vec) {
+          const uint4* bp = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(p.bias) + col0);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          uint32_t bb = 0;
-          if (p.bias != nullptr && col0 + j < p.N) bb = static_cast<const uint32_t*>(p.bias)[col0 + j];
-          o[j] = acc_to_out_bits<OUT>(r[j], bb);
+          for (int q = 0; q < 8; ++q) {
+            const uint4 bv = __ldg(bp + q);
+            o[4 * q + 0] = acc_to_out_bits<OUT>(r[4 * q + 0], bv.x);
+            o[4 * q + 1] = acc_to_out_bits<OUT>(r[4 * q + 1], bv.y);
+            o[4 * q + 2] = acc_to_out_bits<OUT>(r[4 * q + 2], bv.z);
+            o[4 * q + 3] = acc_to_out_bits<OUT>(r[4 * q + 3], bv.w);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const uint32_t bj =
+                (p.bias != nullptr && col0 + j < p.N) ? __ldg(static_cast<const uint32_t*>(p.bias) + col0 + j) : 0u;
+            o[j] = acc_to_out_bits<OUT>(r[j], bj);
+          }
         }
         for (int i = 0; i < p.n_inj; ++i) {
           const gg_injection f = p.inj[i];
@@ -469,87 +526,166 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (row_ok) {
           const long long base = static_cast<long long>(row) * p.ldc + col0;
-          const bool full = (col0 + 32 <= p.N);
           if (p.replay) {
             for (int j = 0; j < 32; ++j)
               if (col0 + j < p.N) changed += (load_out_bits<OUT>(p.C, base + j) != o[j]) ? 1 : 0;
           }
           if (full && vec_ok) {
-            store_chunk_vec<OUT>(static_cast<uint8_t*>(p.C) + base * (OUT <= O_F16 ? 2 : 4), o);
+            store_chunk_vec<OUT>(static_cast<uint8_t*>(p.C) + base * OUT_BYTES, o);
           } else {
             for (int j = 0; j < 32; ++j)
               if (col0 + j < p.N) store_out_bits<OUT>(p.C, base + j, o[j]);
           }
           if constexpr (PROTECT) {
-            // observed row sum of the STORED values, ascending columns
+            // observed row sum of the STORED values (guard.py:170)
+            if constexpr (INT) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (full || col0 + j < p.N) obs += out_bits_to_f64<OUT>(o[j]);
+              for (int j = 0; j < 32; ++j)
+                if (full || col0 + j < p.N) obs_i += static_cast<long long>(static_cast<int>(o[j]));
+            } else if constexpr (OUT == O_F32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (full || col0 + j < p.N) obs += static_cast<double>(__uint_as_float(o[j]));
+            } else {
+              // 16-bit outputs are exact in fp32; fold groups of 8 in fp32, then fp64
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                float s8 = 0.f;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const int j = 8 * g + e;
+                  const float yv = (OUT == O_BF16) ? bf16_bits_to_f32(o[j]) : f16_bits_to_f32(o[j]);
+                  s8 += (full || col0 + j < p.N) ? yv : 0.f;
+                }
+                obs += static_cast<double>(s8);
+              }
+            }
           }
         }
       }
-      // release the TMEM buffer to the MMA warp
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+      if (nchunks <= 0) {  // cannot happen for n < n_tiles; keep the handshake total
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+      }
       if (p.replay && p.changed != nullptr) {
 #pragma unroll
         for (int o2 = 16; o2 > 0; o2 >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o2);
         if (lane == 0 && changed) atomicAdd(p.changed, changed);
       }
       if constexpr (PROTECT) {
-        if (row_ok) p.ws.partial[static_cast<size_t>(n) * p.m_pad + row] = obs;
-        band_arrive(p, m, tid, 1, &gscratch[0]);
+        if (row_ok) {
+          if constexpr (INT) reinterpret_cast<long long*>(p.ws.partial)[static_cast<size_t>(n) * p.m_pad + row] = obs_i;
+          else p.ws.partial[static_cast<size_t>(n) * p.m_pad + row] = obs;
+        }
+        band_arrive<INT>(p, m, tid, 1, &gscratch[0]);
       }
       ++local;
     }
   } else if (warp >= 8) {
     // ================================================= checksum producer side
+    // PREDICTED[m] = sum_k A[m,k] * w_sum[k] (guard.py:168-169), read from the
+    // A stages in shared memory.  The K-blocks of a band are dealt round-robin
+    // to the band's N-tiles (tile n takes kb % n_tiles == n), so every tile
+    // carries 1/n_tiles of the side work and no stage is held long.
     if constexpr (PROTECT) {
       const int tid = threadIdx.x - 256;  // 0..127 == row in tile
+      const int sw = tid & 7;
       int stage = 0;
       uint32_t phase = 0;
-      const double* wsum_f = static_cast<const double*>(p.w_sum);
-      const long long* wsum_i = static_cast<const long long*>(p.w_sum);
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m = t % p.m_tiles, n = t / p.m_tiles;
+        int m, n;
+        tile_coords(p, t, m, n);
         if (!tile_active(m)) continue;
-        const bool designated = (n == 0);
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        double accd = 0.0;                 // bf16/f16/tf32
+        int acc8[3] = {0, 0, 0};           // int8 digit planes (exact)
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&full_bar[stage], phase);
-          if (designated) {
-            const uint8_t* rowp = smA + stage * A_STAGE_BYTES + tid * 128;
-            const int sw = tid & 7;
-            const int kbase = kb * BK;
+          const bool mine = (kb % p.n_tiles) == n;
+          uint4 v[8];
+          if (mine) {
+            // copy this row's 128 B of the stage to registers, then release
+            const uint32_t rowaddr = smem_u32(smA + stage * A_STAGE_BYTES) + static_cast<uint32_t>(tid * 128);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint4 v = *reinterpret_cast<const uint4*>(rowp + ((j ^ sw) << 4));
-              const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-              constexpr int PER = 16 / T::ELEM;  // elements per 16 B chunk
-#pragma unroll
-              for (int e = 0; e < PER; ++e) {
-                const int k = kbase + j * PER + e;
-                double x;
-                if constexpr (KIND == K_BF16) x = bf16_bits_to_f32((w4[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
-                else if constexpr (KIND == K_F16) x = f16_bits_to_f32((w4[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
-                else if constexpr (KIND == K_TF32) x = __uint_as_float(w4[e]);
-                else x = static_cast<double>(static_cast<int8_t>((w4[e >> 2] >> (8 * (e & 3))) & 0xFFu));
-                double w = 0.0;
-                if (k < p.K) w = p.chk_int ? static_cast<double>(__ldg(&wsum_i[k])) : __ldg(&wsum_f[k]);
-                acc[e & 3] = fma(x, w, acc[e & 3]);
-              }
-            }
+            for (int j = 0; j < 8; ++j) v[j] = lds128(rowaddr + static_cast<uint32_t>((j ^ sw) << 4));
+            // WAR across proxies: these generic-proxy reads must be ordered before
+            // the async-proxy (TMA) refill the empty-barrier arrival enables.
+            fence_proxy_async_smem();
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (!mine) continue;
+          const int kbase = kb * BK;
+          const bool tail = kbase + BK > p.K;  // warp-uniform; TMA zero-fills x beyond K
+          if constexpr (INT) {
+            // sum_k x*w = sum_d 256^d * sum_k x*digit_d(w): IDP4A, exact in int32
+            const int4* dig = static_cast<const int4*>(p.w_aux) + (kbase >> 2);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int kq = kbase + j * 16 + q * 4;
+                int4 dd = make_int4(0, 0, 0, 0);
+                if (!tail || kq < p.K) dd = __ldg(dig + j * 4 + q);
+                acc8[0] = __dp4a(static_cast<int>(w4[q]), dd.x, acc8[0]);
+                acc8[1] = __dp4a(static_cast<int>(w4[q]), dd.y, acc8[1]);
+                acc8[2] = __dp4a(static_cast<int>(w4[q]), dd.z, acc8[2]);
+              }
+            }
+          } else if constexpr (KIND == K_TF32) {
+            // fp32 operands: full fp64 products (x exact in double)
+            const double* wf = static_cast<const double*>(p.w_sum);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int k = kbase + j * 4 + e;
+                const double w = (!tail || k < p.K) ? __ldg(wf + k) : 0.0;
+                accd = fma(static_cast<double>(__uint_as_float(w4[e])), w, accd);
+              }
+            }
+          } else {
+            // bf16/f16: x is exact in fp32; w_sum = hi + lo (two fp32); fp32 FMAs
+            // over 16-element groups, folded into fp64 once per group.
+            const float2* w2 = static_cast<const float2*>(p.w_aux) + kbase;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              float sh = 0.f, sl = 0.f;
+#pragma unroll
+              for (int jj = 0; jj < 2; ++jj) {
+                const int j = 2 * g + jj;
+                const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const int k = j * 8 + e;
+                  const uint32_t h = (w4[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+                  float x;
+                  if constexpr (KIND == K_BF16) x = bf16_bits_to_f32(h);
+                  else x = f16_bits_to_f32(h);
+                  float2 w = make_float2(0.f, 0.f);
+                  if (!tail || kbase + k < p.K) w = __ldg(w2 + k);
+                  sh = fmaf(x, w.x, sh);
+                  sl = fmaf(x, w.y, sl);
+                }
+              }
+              accd += static_cast<double>(sh);
+              accd += static_cast<double>(sl);
+            }
+          }
         }
-        if (designated) {
-          const int row = m * BM + tid;
-          if (row < p.M) p.ws.pred[row] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-          band_arrive(p, m, tid, 2, &gscratch[1]);
+        const int row = m * BM + tid;
+        if (row < p.M) {
+          if constexpr (INT) {
+            const long long pr = static_cast<long long>(acc8[0]) + 256ll * acc8[1] + 65536ll * acc8[2];
+            reinterpret_cast<long long*>(p.ws.pred)[static_cast<size_t>(n) * p.m_pad + row] = pr;
+          } else {
+            p.ws.pred[static_cast<size_t>(n) * p.m_pad + row] = accd;
+          }
         }
+        band_arrive<INT>(p, m, tid, 2, &gscratch[1]);
       }
     }
   }

@@ -47,6 +47,9 @@ int launch_gemm_exact(int dtype, int accum, const void* X, int64_t M, int64_t K,
 int launch_reduce(int dtype, const void* A, int64_t rows, int64_t cols, int axis, void* out, cudaStream_t s);
 int launch_round(int dtype, const double* in, void* out, int64_t n, cudaStream_t s);
 
+size_t checksum_aux_bytes(int ab_kind, int64_t K);
+int launch_checksum_aux(int ab_kind, const void* w_sum, int64_t K, void* aux, cudaStream_t s);
+
 // implemented in gg_gemm_sm100.cu
 size_t protected_gemm_workspace_bytes(int64_t M, int64_t N);
 int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s);

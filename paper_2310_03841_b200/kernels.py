@@ -135,6 +135,7 @@ def build_desc(
     *,
     protect: bool,
     w_sum: torch.Tensor | None = None,
+    w_aux: torch.Tensor | None = None,
     bias_sum: float | int = 0,
     mu: float = 0.0,
     lo: float = 0.0,
@@ -162,6 +163,7 @@ def build_desc(
     d.chk_prec = L.GG_P_I64 if integer else L.GG_P_F64
     if protect:
         d.w_sum = _ptr(w_sum)
+        d.w_aux = _ptr(w_aux)
         if integer:
             d.bias_sum_i = int(bias_sum)
         else:
@@ -179,6 +181,21 @@ def build_desc(
     d.replay_rows = _ptr(replay_rows)
     d.changed = _ptr(changed)
     return d
+
+
+def checksum_aux(w_sum: torch.Tensor, ab_dtype: torch.dtype) -> torch.Tensor | None:
+    """Side-path encoding of w_sum for the fused checksum (gg_checksum_aux):
+    (hi, lo) fp32 split for bf16/fp16 operands, signed digit planes for int8,
+    None for fp32 (tf32) operands.  Computed once per weight."""
+    dev = _require_cuda(w_sum)
+    kind = TORCH_TO_GG[ab_dtype]
+    K = w_sum.numel()
+    nbytes = int(L.load().gg_checksum_aux_bytes(kind, K))
+    if nbytes == 0:
+        return None
+    aux = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    L.check(L.load().gg_checksum_aux(kind, w_sum.data_ptr(), K, aux.data_ptr(), _stream(dev)), "gg_checksum_aux")
+    return aux
 
 
 def _check_gemm_operands(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None):
@@ -210,6 +227,7 @@ def protected_gemm(
     out_dtype: torch.dtype | None = None,
     protect: bool = True,
     w_sum: torch.Tensor | None = None,
+    w_aux: torch.Tensor | None = None,
     bias_sum: float | int = 0,
     mu: float = 0.0,
     lo: float = 0.0,
@@ -235,6 +253,8 @@ def protected_gemm(
     if protect:
         if w_sum is None:
             raise ValueError("protect=True needs the offline checksum w_sum")
+        if w_aux is None:
+            w_aux = checksum_aux(w_sum, x.dtype)
         result = result or CheckResult.empty(M, x.dtype == torch.int8, dev)
         ws = workspace(M, N, dev, ws_key)
     else:
@@ -245,8 +265,8 @@ def protected_gemm(
         inj_dev, n_inj = injections_to_device(injections, dev), len(injections)
     else:
         inj_dev, n_inj = None, 0
-    desc = build_desc(x, w, y, bias, protect=protect, w_sum=w_sum, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
-                      statistic=statistic, result=result, inj_dev=inj_dev, n_inj=n_inj, ws=ws)
+    desc = build_desc(x, w, y, bias, protect=protect, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo,
+                      hi=hi, statistic=statistic, result=result, inj_dev=inj_dev, n_inj=n_inj, ws=ws)
     L.check(L.load().gg_protected_gemm(ctypes.byref(desc), _stream(dev)), "gg_protected_gemm")
     return y, (result if protect else None)
 
@@ -260,6 +280,7 @@ def replay_tiles(
     result: CheckResult,
     *,
     w_sum: torch.Tensor,
+    w_aux: torch.Tensor | None = None,
     bias_sum: float | int = 0,
     mu: float = 0.0,
     lo: float = 0.0,
@@ -280,7 +301,9 @@ def replay_tiles(
     M, N = x.shape[0], w.shape[0]
     changed = changed if changed is not None else torch.zeros(1, dtype=torch.int32, device=dev)
     ws = workspace(M, N, dev, ws_key)
-    desc = build_desc(x, w, y, bias, protect=True, w_sum=w_sum, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
+    if w_aux is None:
+        w_aux = checksum_aux(w_sum, x.dtype)
+    desc = build_desc(x, w, y, bias, protect=True, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
                       statistic=statistic, result=result, ws=ws, replay_rows=replay_rows, changed=changed)
     L.check(L.load().gg_replay_tiles(ctypes.byref(desc), _stream(dev)), "gg_replay_tiles")
     return changed

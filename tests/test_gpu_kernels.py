@@ -69,14 +69,20 @@ def test_protected_checksum_matches_fp64(dtype, shape):
     if integer:
         pred = x.cpu().long() @ w_sum.cpu() + int(bsum.item())
         obs = y.cpu().long().sum(1)
-        assert torch.equal(res.d.cpu(), pred - obs)
+        bad = torch.nonzero(res.d.cpu() != pred - obs).flatten()
+        assert bad.numel() == 0, (bad[:10].tolist(), res.d.cpu()[bad[:5]].tolist(), (pred - obs)[bad[:5]].tolist(),
+                                  (x.cpu().long() @ w_sum.cpu())[bad[:5]].tolist(), obs[bad[:5]].tolist())
         assert int(res.nflag.item()) == int((pred != obs).sum())
     else:
         pred = x.double() @ w_sum + bsum.double()
         obs = y.double().sum(1)
         d_ref = (pred - obs).cpu()
         mag = ((x.double().abs() @ w_sum.abs()) + y.double().abs().sum(1)).cpu()
-        assert bool(((res.d.cpu() - d_ref).abs() <= mag * 1e-13 + 1e-300).all())
+        # bf16/fp16: fp32 group sums (16 products / 8 outputs) folded in fp64,
+        # error <= 2^-20 * sum|terms|; tf32: fp64 throughout.
+        rel = 2.0**-20 if dtype in (torch.bfloat16, torch.float16) else 1e-13
+        err = (res.d.cpu() - d_ref).abs()
+        assert bool((err <= mag * rel + 1e-300).all()), (float(err.max()), float((err / mag).max()))
         assert int(res.nflag.item()) == 0 and int(res.triggered.item()) == 0
         gap = (res.d.cpu()).abs().max().item()
         assert abs(res.max_disc.item() - gap) <= 1e-12 * max(gap, 1e-300)

@@ -21,11 +21,11 @@ for dt in [torch.bfloat16, torch.int8, torch.float16, torch.float32]:
         else:
             x=torch.randn(M,Kd,device='cuda').to(dt); w=(torch.randn(N,Kd,device='cuda')/Kd**.5).to(dt); b=torch.zeros(N,device='cuda')
             prec=L.GG_P_F64
-        ws,bs=K.offline_checksum(w,b,prec)
+        ws,bs=K.offline_checksum(w,b,prec); aux=K.checksum_aux(ws,dt)
         y=torch.empty(M,N,dtype=K.default_out_dtype(dt),device='cuda')
         res=K.CheckResult.empty(M,dt==torch.int8,'cuda')
         tu=t(lambda: K.protected_gemm(x,w,b,protect=False,out=y))
-        tp=t(lambda: K.protected_gemm(x,w,b,w_sum=ws,bias_sum=bs.item(),lo=-1e30,hi=1e30,out=y,result=res))
+        bsv=bs.item(); tp=t(lambda: K.protected_gemm(x,w,b,w_sum=ws,w_aux=aux,bias_sum=bsv,lo=-1e30,hi=1e30,out=y,result=res))
         fl=2*M*N*Kd
         ref=None
         if dt!=torch.int8:
