@@ -296,29 +296,24 @@ __global__ void flip_bits_kernel(uint8_t* base, int elem_bytes, const int64_t* e
 // rounded to the operand dtype.  numerics._gemm_accumulate starts the fold at
 // the first product when B*I*O <= 2^26 (np.add.accumulate) and at zero
 // otherwise (the k-loop path); both are reproduced (start_zero).
-template <class A, int OUT_DT>
+template <class A>
 __global__ void gemm_exact_kernel(int dtype, const void* X, int64_t M, int64_t K, const void* Wt, int64_t N,
                                   const void* bias, void* Y, bool start_zero) {
   const int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t b = blockIdx.y;
-  if (o >= N || b >= M) return;
+  if (o >= N) return;
   using T = typename A::T;
-  T acc;
-  int64_t k0;
-  if (start_zero) {
-    acc = T(0);
-    k0 = 0;
-  } else {
-    acc = A::mul(A::from(X, dtype, b * K), A::from(Wt, dtype, o));
-    k0 = 1;
-  }
-  for (int64_t k = k0; k < K; ++k) acc = A::add(acc, A::mul(A::from(X, dtype, b * K + k), A::from(Wt, dtype, k * N + o)));
-  if constexpr (std::is_same<A, AccI64>::value) {
-    // integer path is int32 with wrap-around (numerics.py:267-272)
-    int32_t r = static_cast<int32_t>(acc);
-    if (bias) r = static_cast<int32_t>(static_cast<uint32_t>(r) + static_cast<uint32_t>(static_cast<const int32_t*>(bias)[o]));
-    static_cast<int32_t*>(Y)[b * N + o] = r;
-  } else {
+  for (int64_t b = blockIdx.y; b < M; b += gridDim.y) {
+    T acc;
+    int64_t k0;
+    if (start_zero) {
+      acc = T(0);
+      k0 = 0;
+    } else {
+      acc = A::mul(A::from(X, dtype, b * K), A::from(Wt, dtype, o));
+      k0 = 1;
+    }
+    for (int64_t k = k0; k < K; ++k)
+      acc = A::add(acc, A::mul(A::from(X, dtype, b * K + k), A::from(Wt, dtype, k * N + o)));
     if (bias) acc = A::add(acc, A::from(bias, GG_F64, o));  // bias.astype(acc)
     const double v = A::to_f64(acc);
     if (dtype == GG_F64) static_cast<double*>(Y)[b * N + o] = v;
@@ -328,26 +323,27 @@ __global__ void gemm_exact_kernel(int dtype, const void* X, int64_t M, int64_t K
   }
 }
 // int32 accumulation for integer operands: products and sums wrap in int32
+// (X.astype(int32) * Wt.astype(int32), numerics.py:267-272).
 struct AccI32 {
   using T = int;
-  __device__ static T from(const void* b, int dt, int64_t i) { return static_cast<T>(load_as_i64(b, dt, i)); }
   __device__ static T add(T a, T b) { return static_cast<T>(static_cast<unsigned>(a) + static_cast<unsigned>(b)); }
   __device__ static T mul(T a, T b) { return static_cast<T>(static_cast<unsigned>(a) * static_cast<unsigned>(b)); }
 };
-__global__ void gemm_exact_int_kernel(const void* X, int64_t M, int64_t K, const void* Wt, int64_t N,
-                                      const int32_t* bias, int32_t* Y, bool start_zero) {
+template <typename E>
+__global__ void gemm_exact_int_kernel(const E* x, int64_t M, int64_t K, const E* w, int64_t N, const int32_t* bias,
+                                      int32_t* Y, bool start_zero) {
   const int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t b = blockIdx.y;
-  if (o >= N || b >= M) return;
-  const int8_t* x = static_cast<const int8_t*>(X);
-  const int8_t* w = static_cast<const int8_t*>(Wt);
-  int acc;
-  int64_t k0;
-  if (start_zero) { acc = 0; k0 = 0; }
-  else { acc = static_cast<int>(x[b * K]) * static_cast<int>(w[o]); k0 = 1; }
-  for (int64_t k = k0; k < K; ++k) acc = AccI32::add(acc, static_cast<int>(x[b * K + k]) * static_cast<int>(w[k * N + o]));
-  if (bias) acc = AccI32::add(acc, bias[o]);
-  Y[b * N + o] = acc;
+  if (o >= N) return;
+  for (int64_t b = blockIdx.y; b < M; b += gridDim.y) {
+    int acc;
+    int64_t k0;
+    if (start_zero) { acc = 0; k0 = 0; }
+    else { acc = AccI32::mul(static_cast<int>(x[b * K]), static_cast<int>(w[o])); k0 = 1; }
+    for (int64_t k = k0; k < K; ++k)
+      acc = AccI32::add(acc, AccI32::mul(static_cast<int>(x[b * K + k]), static_cast<int>(w[k * N + o])));
+    if (bias) acc = AccI32::add(acc, bias[o]);
+    Y[b * N + o] = acc;
+  }
 }
 
 // ------------------------------------------------------------ reductions
@@ -487,25 +483,33 @@ int launch_flip_bits(void* ptr, int elem_bytes, const int64_t* elem_idx, const i
 int launch_gemm_exact(int dtype, int accum, const void* X, int64_t M, int64_t K, const void* Wt, int64_t N,
                       const void* bias, void* Y, cudaStream_t s) {
   if (M < 1 || K < 1 || N < 1) return fail(GG_EINVAL, "gemm dims mismatch: empty operand");
-  if (M > 65535) return fail(GG_EINVAL, "gemm_exact: M > 65535 rows is not supported");
   const bool start_zero = (M * K * N) > (int64_t(1) << 26);  // numerics.py:219,225
-  dim3 grid(grid1(N, 128), static_cast<unsigned>(M));
-  const bool is_int = (dtype == GG_I8);
-  if (is_int) {
+  dim3 grid(grid1(N, 128), static_cast<unsigned>(M < 65535 ? M : 65535));
+  if (dtype == GG_I8 || dtype == GG_I32) {
     if (accum != GG_P_I64) return fail(GG_EINVAL, "integer gemm requires the int64-exact accumulation tag");
-    gemm_exact_int_kernel<<<grid, 128, 0, s>>>(X, M, K, Wt, N, static_cast<const int32_t*>(bias),
-                                               static_cast<int32_t*>(Y), start_zero);
+    if (dtype == GG_I8)
+      gemm_exact_int_kernel<int8_t><<<grid, 128, 0, s>>>(static_cast<const int8_t*>(X), M, K,
+                                                         static_cast<const int8_t*>(Wt), N,
+                                                         static_cast<const int32_t*>(bias), static_cast<int32_t*>(Y),
+                                                         start_zero);
+    else
+      gemm_exact_int_kernel<int32_t><<<grid, 128, 0, s>>>(static_cast<const int32_t*>(X), M, K,
+                                                          static_cast<const int32_t*>(Wt), N,
+                                                          static_cast<const int32_t*>(bias),
+                                                          static_cast<int32_t*>(Y), start_zero);
     return check_launch("gemm_exact");
   }
+  if (dtype != GG_F64 && dtype != GG_F32 && dtype != GG_F16 && dtype != GG_BF16)
+    return fail(GG_EINVAL, "gemm_exact: unsupported operand dtype");
   if (accum == GG_P_I64) return fail(GG_EINVAL, "float gemm requires a floating accumulation precision");
   const int width = dtype == GG_F64 ? 64 : dtype == GG_F32 ? 32 : 16;
   const int awidth = accum == GG_P_F64 ? 64 : accum == GG_P_F32 ? 32 : 16;
   if (awidth < width) return fail(GG_EINVAL, "accumulation narrower than operand dtype");
   if (dtype == GG_F16 && awidth < 32) return fail(GG_EINVAL, "binary16-emulated gemm accumulates in binary32 or wider");
   if (accum == GG_P_F64)
-    gemm_exact_kernel<AccF64, 0><<<grid, 128, 0, s>>>(dtype, X, M, K, Wt, N, bias, Y, start_zero);
+    gemm_exact_kernel<AccF64><<<grid, 128, 0, s>>>(dtype, X, M, K, Wt, N, bias, Y, start_zero);
   else
-    gemm_exact_kernel<AccF32, 0><<<grid, 128, 0, s>>>(dtype, X, M, K, Wt, N, bias, Y, start_zero);
+    gemm_exact_kernel<AccF32><<<grid, 128, 0, s>>>(dtype, X, M, K, Wt, N, bias, Y, start_zero);
   return check_launch("gemm_exact");
 }
 

@@ -386,7 +386,7 @@ def gemm_exact(x: torch.Tensor, wt: torch.Tensor, bias: torch.Tensor | None, acc
     wt = wt.contiguous()
     M, K = x.shape
     N = wt.shape[1]
-    odt = torch.int32 if x.dtype == torch.int8 else x.dtype
+    odt = torch.int32 if x.dtype in (torch.int8, torch.int32) else x.dtype
     y = torch.empty((M, N), dtype=odt, device=dev)
     b = None if bias is None else bias.contiguous()
     L.check(
