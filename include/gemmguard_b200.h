@@ -155,14 +155,14 @@ GG_API int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_
                         void* bias_sum_out, void* stream);
 
 /* Side-path encoding of w_sum consumed by the fused checksum of K1, computed
- * once per weight (offline, like w_sum itself):
- *   GG_BF16 / GG_F16: float2 [K] = (hi, lo) with hi = fp32(w_sum),
- *                     lo = fp32(w_sum - hi), so x*w_sum is formed with fp32
- *                     FMAs and folded into fp64 every 16 products;
- *   GG_I8:            int32x4 [ceil(K/4)] signed base-256 digit planes of the
- *                     int64 w_sum (|w_sum| < 2^23), so x*w_sum is an exact
- *                     IDP4A dot product;
- *   GG_F32:           none (0 bytes; the tf32 path reads w_sum directly). */
+ * once per weight (offline, like w_sum itself), zero-padded to a multiple of
+ * 128 K-elements so the kernel reads whole K-blocks:
+ *   GG_BF16 / GG_F16: float [Kp]  = fp32(w_sum); bf16/fp16 x are exact in fp32,
+ *                     so x*w is one fp32 FMA (|w - w_sum| <= 2^-24 |w_sum|),
+ *                     folded into fp64 once per K-block of 64;
+ *   GG_F32 (tf32):    double [Kp] = w_sum (fp64 products of the fp32 x);
+ *   GG_I8:            int32x4 [Kp/4] signed base-256 digit planes of the int64
+ *                     w_sum (|w_sum| < 2^23), so x*w_sum is an exact IDP4A dot. */
 GG_API size_t gg_checksum_aux_bytes(int32_t ab_kind, int64_t K);
 GG_API int gg_checksum_aux(int32_t ab_kind, const void* w_sum, int64_t K, void* aux_out,
                            void* stream);

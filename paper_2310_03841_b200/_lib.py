@@ -12,7 +12,9 @@ import ctypes
 from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_uint8, c_void_p
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libgemmguard_b200.so"
+import os
+
+LIB_PATH = Path(os.environ.get("GEMMGUARD_LIB", Path(__file__).resolve().parent / "libgemmguard_b200.so"))
 
 # enum gg_dtype
 GG_F64, GG_F32, GG_F16, GG_BF16, GG_I8, GG_I32, GG_I64 = range(7)

@@ -376,17 +376,24 @@ __global__ void round_kernel(int dtype, const double* in, void* out, int64_t n) 
 }
 
 // w_sum side-path encodings for the fused checksum (see gg_checksum_aux).
-__global__ void split_f64_kernel(const double* w, int64_t K, float2* out) {
+// Every encoding is zero-padded to a multiple of 128 K-elements so the GEMM's
+// checksum warps read whole K-blocks without bounds checks.
+constexpr int64_t AUX_PAD = 128;
+inline int64_t aux_padded(int64_t K) { return (K + AUX_PAD - 1) / AUX_PAD * AUX_PAD; }
+
+__global__ void f32_of_f64_kernel(const double* w, int64_t K, int64_t Kp, float* out) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k >= K) return;
-  const double v = w[k];
-  const float hi = __double2float_rn(v);
-  const float lo = __double2float_rn(v - static_cast<double>(hi));
-  out[k] = make_float2(hi, lo);
+  if (k >= Kp) return;
+  out[k] = k < K ? __double2float_rn(w[k]) : 0.f;
 }
-__global__ void digits_i64_kernel(const long long* w, int64_t K, int4* out) {
+__global__ void f64_copy_kernel(const double* w, int64_t K, int64_t Kp, double* out) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= Kp) return;
+  out[k] = k < K ? w[k] : 0.0;
+}
+__global__ void digits_i64_kernel(const long long* w, int64_t K, int64_t Kp, int4* out) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // group of 4 k
-  if (i * 4 >= K) return;
+  if (i * 4 >= Kp) return;
   uint32_t plane[3] = {0u, 0u, 0u};
   for (int e = 0; e < 4; ++e) {
     const int64_t k = i * 4 + e;
@@ -515,25 +522,31 @@ int launch_gemm_exact(int dtype, int accum, const void* X, int64_t M, int64_t K,
 
 size_t checksum_aux_bytes(int ab_kind, int64_t K) {
   if (K < 1) return 0;
+  const int64_t Kp = aux_padded(K);
   switch (ab_kind) {
-    case GG_BF16: case GG_F16: return static_cast<size_t>(K) * 8;
-    case GG_I8: return static_cast<size_t>((K + 3) / 4) * 16;
+    case GG_BF16: case GG_F16: return static_cast<size_t>(Kp) * 4;
+    case GG_F32: return static_cast<size_t>(Kp) * 8;
+    case GG_I8: return static_cast<size_t>(Kp / 4) * 16;
     default: return 0;
   }
 }
 
 int launch_checksum_aux(int ab_kind, const void* w_sum, int64_t K, void* aux, cudaStream_t s) {
   if (K < 1) return fail(GG_EINVAL, "checksum_aux: empty w_sum");
+  const int64_t Kp = aux_padded(K);
   switch (ab_kind) {
     case GG_BF16: case GG_F16:
-      split_f64_kernel<<<grid1(K, 256), 256, 0, s>>>(static_cast<const double*>(w_sum), K, static_cast<float2*>(aux));
-      break;
-    case GG_I8:
-      digits_i64_kernel<<<grid1((K + 3) / 4, 256), 256, 0, s>>>(static_cast<const long long*>(w_sum), K,
-                                                              static_cast<int4*>(aux));
+      f32_of_f64_kernel<<<grid1(Kp, 256), 256, 0, s>>>(static_cast<const double*>(w_sum), K, Kp,
+                                                       static_cast<float*>(aux));
       break;
     case GG_F32:
-      return 0;
+      f64_copy_kernel<<<grid1(Kp, 256), 256, 0, s>>>(static_cast<const double*>(w_sum), K, Kp,
+                                                     static_cast<double*>(aux));
+      break;
+    case GG_I8:
+      digits_i64_kernel<<<grid1(Kp / 4, 256), 256, 0, s>>>(static_cast<const long long*>(w_sum), K, Kp,
+                                                           static_cast<int4*>(aux));
+      break;
     default:
       return fail(GG_EINVAL, "checksum_aux: unknown ab_kind");
   }

@@ -1,0 +1,780 @@
+// gg_gemm2_sm100.cuh — K1/K4: checksum-protected GEMM on CTA pairs (sm_100a).
+//
+//   C[m, n] = sum_k A[m, k] * B[n, k] + bias[n]          (tcgen05.mma.cta_group::2)
+//   d[m]    = (sum_k A[m, k] * w_sum[k] + bias_sum) - sum_n C[m, n]
+//   flags   = guard._verify_arrays rule on d            (guard.py:188-215)
+//
+// A cluster of two CTAs on the two SMs of a TPC computes 256 x 256 tiles: each
+// CTA stages 128 rows of A and 128 rows (N) of B per K-block, the leader issues
+// one M=256, N=256 MMA reading both CTAs' shared memory, and each CTA's TMEM
+// holds the fp32/s32 accumulators of its own 128 rows (two 256-column buffers:
+// the epilogue of tile i overlaps the mainloop of tile i+1).
+//
+// Tile schedule: the pair tiles (256-row band m, 256-column tile n; n fastest)
+// are cut into one CONTIGUOUS range per pair, so a pair walks whole row bands
+// and folds their checksums locally; only a band cut by a range boundary
+// exchanges partials through global memory.  When the A bands streamed by all
+// pairs at once would not fit in L2 (long K), pairs walk the tiles strided
+// instead (neighbouring pairs share A bands in L2) and every band exchanges
+// its partials through global memory.
+//
+// Warp roles (384 threads per CTA):
+//   0      TMA producer (both CTAs; loads complete on the LEADER's full barrier)
+//   1      MMA issuer (leader only, one thread): stage release and
+//          accumulator hand-off are tcgen05.commit multicasts to both CTAs.
+//   2      TMEM allocator (both CTAs, cta_group::2)
+//   3      reducer: folds the per-tile row partials of each band (registers
+//          for local bands, global partials + one fence for split bands),
+//          writes d / flags and the launch summaries
+//   8-11   epilogue: TMEM -> registers, bias, round, fault injection,
+//          OBSERVED row sums over the stored values (guard.py:170), then a
+//          32x32 swizzled smem box per warp and a TMA store (coalesced C).
+//          Highest warp ids: the SMSP arbiter issues highest-id-first, so the
+//          critical-path warps win every issue tie.
+//   4-7    checksum producer side: PREDICTED[m] = A[m,:] . w_sum (guard.py:
+//          168-169) from the A stages already in shared memory.  A band's
+//          K-blocks are dealt round-robin over its N-tiles; the MMA thread
+//          relays "owned stage landed" (local + remote mbarrier arrive) before
+//          issuing that stage's MMAs, the checksum warps copy their row to
+//          registers at once and release the stage, so the refill of an owned
+//          stage is not delayed.
+// Everything is deterministic (fixed fold orders, no float atomics), so a
+// recompute is byte-identical — required by replay (guard.py:590).
+#pragma once
+#include "gg_gemm_sm100.cuh"
+
+namespace gg {
+namespace pair {
+
+// Diagnostics: with -DGG_TRACE the roles stamp clock64() per tile into a
+// device buffer (gg_trace_buffer); compiled out of the production library.
+#ifdef GG_TRACE
+__device__ unsigned long long* g_trace = nullptr;
+constexpr int TRACE_TILES = 64, TRACE_EV = 20;
+#define GG_EV(ev, local)                                                                                  \
+  do {                                                                                                  \
+    if (g_trace != nullptr && (local) < TRACE_TILES)                                                    \
+      g_trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + (local)) * TRACE_EV + (ev)] = clock64(); \
+  } while (0)
+#else
+#define GG_EV(ev, local) \
+  do {                   \
+  } while (0)
+#endif
+
+constexpr int BM = 128;           // rows per CTA (256 per pair)
+constexpr int BN = 256;           // MMA N per tile; each CTA stages BN/2 rows of B
+constexpr int BK_BYTES = 128;     // one 128 B swizzle atom of K per stage
+constexpr int STAGES = 5;
+constexpr int THREADS = 384;
+constexpr int A_BYTES = BM * BK_BYTES;        // 16 KB
+constexpr int B_BYTES = (BN / 2) * BK_BYTES;  // 16 KB
+constexpr int TMEM_COLS = 2 * BN;
+constexpr int CBOX = 32;                      // epilogue store box: 32 rows x 32 columns per warp
+constexpr int CST_BYTES = CBOX * CBOX * 4;    // 4 KB staging per box (2 KB used by 16-bit outputs)
+constexpr int C_OFF = STAGES * (A_BYTES + B_BYTES);
+constexpr int BAR_OFF = C_OFF + 4 * 2 * CST_BYTES;
+constexpr int NSLOT = 4;                      // depth of the observed / predicted partial rings
+constexpr int NBAR = 4 * STAGES + 4 + 4 * NSLOT;
+constexpr int SMEM_BYTES = BAR_OFF + NBAR * 8 + 16 /*tmem slot*/ + 2 * NSLOT * BM * 8 /*partial rings*/ +
+                           2 * BN * 4 /*bias tiles*/ + 1024 /*align*/;
+
+template <int KIND> struct PairIdesc;
+template <> struct PairIdesc<K_BF16> { static constexpr uint32_t V = make_idesc(1, 1, 256, BN); };
+template <> struct PairIdesc<K_F16> { static constexpr uint32_t V = make_idesc(1, 0, 256, BN); };
+template <> struct PairIdesc<K_TF32> { static constexpr uint32_t V = make_idesc(1, 2, 256, BN); };
+template <> struct PairIdesc<K_I8> { static constexpr uint32_t V = make_idesc(2, 1, 256, BN); };
+
+// Contiguous tile range of pair `pid` out of `npairs` over `total` tiles.
+__device__ __forceinline__ void pair_range(int pid, int npairs, int total, int& t0, int& t1) {
+  t0 = static_cast<int>(static_cast<long long>(pid) * total / npairs);
+  t1 = static_cast<int>(static_cast<long long>(pid + 1) * total / npairs);
+}
+
+// d / flags of the rows lane + 32q (q < 4) of band mb from their folded sums,
+// then the band summary and, for the last band of the launch, the launch
+// summaries (nflag, triggered, max_disc).  One warp.
+template <bool INT>
+__device__ void finish_band(const Params& p, int mb, int lane, const double (&obs_f)[4], const double (&pred_f)[4],
+                            const long long (&obs_i)[4], const long long (&pred_i)[4]) {
+  int nflag = 0;
+  unsigned long long key = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int row = mb * BM + lane + 32 * q;
+    if (row >= p.M) continue;
+    bool flag;
+    if constexpr (INT) {
+      const long long di = (pred_i[q] + p.bias_sum_i) - obs_i[q];
+      static_cast<long long*>(p.d)[row] = di;
+      flag = di != 0;
+      const unsigned long long mag =
+          di < 0 ? 0ull - static_cast<unsigned long long>(di) : static_cast<unsigned long long>(di);
+      const unsigned long long k = gap_key(static_cast<double>(mag));
+      key = k > key ? k : key;
+    } else {
+      const double dd = (pred_f[q] + p.bias_sum_f) - obs_f[q];
+      static_cast<double*>(p.d)[row] = dd;
+      flag = !((dd >= p.lo) && (dd <= p.hi));
+      const unsigned long long k = gap_key(fabs(dd - p.mu));
+      key = k > key ? k : key;
+    }
+    if (INT || p.statistic == GG_PER_SAMPLE) {
+      p.flags[row] = flag ? 1 : 0;
+      nflag += flag ? 1 : 0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nflag += __shfl_xor_sync(0xffffffffu, nflag, o);
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, key, o);
+    key = w > key ? w : key;
+  }
+  int last = 0;
+  if (lane == 0) {
+    p.ws.band_nflag[mb] = nflag;
+    p.ws.band_maxkey[mb] = key;
+  }
+  __syncwarp();
+  __threadfence();  // this band's d / flags / summary before the launch-level count (one fence per band)
+  if (lane == 0) {
+    const int total = p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles;
+    last = (atomicAdd(&p.ws.counters[0], 1) == total - 1) ? 1 : 0;
+    if (last) __threadfence();
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  int nf = 0;
+  unsigned long long mk = 0;
+  for (int b = lane; b < p.m_tiles; b += 32) {
+    nf += __ldcg(&p.ws.band_nflag[b]);
+    const unsigned long long k = __ldcg(&p.ws.band_maxkey[b]);
+    mk = k > mk ? k : mk;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nf += __shfl_xor_sync(0xffffffffu, nf, o);
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mk, o);
+    mk = w > mk ? w : mk;
+  }
+  if (!INT && p.statistic == GG_BATCH_MEAN) {
+    double s = 0.0;  // fixed lane -> row assignment and shuffle tree: deterministic
+    for (int r = lane; r < p.M; r += 32) s += ldcg_f64(&static_cast<double*>(p.d)[r]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double dm = s / static_cast<double>(p.M);
+    const bool inside = (p.lo <= dm) && (dm <= p.hi);
+    for (int r = lane; r < p.M; r += 32) p.flags[r] = inside ? 0 : 1;
+    nf = inside ? 0 : p.M;
+  }
+  if (lane == 0) {
+    *p.nflag = nf;
+    *p.triggered = nf > 0 ? 1 : 0;
+    *p.max_disc = (mk == 0ull) ? __longlong_as_double(0x7FF0000000000000ll)
+                               : __longlong_as_double(static_cast<long long>(mk - 1ull));
+    p.ws.counters[0] = 0;
+    __threadfence();
+  }
+}
+
+// Write the 32 output encodings of this thread's box row into the swizzled staging box.
+template <int OUT>
+__device__ __forceinline__ void stage_row(uint32_t box, int lane, const uint32_t (&o)[32]) {
+  if constexpr (OUT == O_BF16 || OUT == O_F16) {
+    const uint32_t row = box + static_cast<uint32_t>(lane * 64);  // SWIZZLE_64B: chunk ^= (row >> 1) & 3
+    const int sw = (lane >> 1) & 3;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)  // o[] holds packed pairs
+      sts128(row + static_cast<uint32_t>((c ^ sw) << 4), o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+  } else {
+    const uint32_t row = box + static_cast<uint32_t>(lane * 128);  // SWIZZLE_128B: chunk ^= row & 7
+    const int sw = lane & 7;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      sts128(row + static_cast<uint32_t>((c ^ sw) << 4), o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+  }
+}
+
+template <int KIND, int OUT, bool PROTECT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gg_protected_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                                  const __grid_constant__ CUtensorMap tmC, const Params p) {
+  using T = KindTraits<KIND>;
+  constexpr bool INT = (KIND == K_I8);
+  constexpr int BK = BK_BYTES / T::ELEM;
+  constexpr int MMA_K_BYTES = 32;
+  constexpr int MMAS_PER_STAGE = BK_BYTES / MMA_K_BYTES;
+  constexpr bool OUT16 = (OUT == O_BF16 || OUT == O_F16);
+  constexpr uint32_t IDESC = PairIdesc<KIND>::V;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * A_BYTES;
+  uint8_t* smC = smem + C_OFF;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* aready_bar = empty_bar + STAGES;    // owned stage has landed (relayed by the MMA thread)
+  uint64_t* chkdone_bar = aready_bar + STAGES;  // checksum warps copied an owned stage
+  uint64_t* tfull_bar = chkdone_bar + STAGES;   // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;         // [2] leader: the pair's 8 epilogue warps
+  uint64_t* ofull_bar = tempty_bar + 2;         // [NSLOT] observed partials of a tile ready (4 epilogue warps)
+  uint64_t* oempty_bar = ofull_bar + NSLOT;     // [NSLOT] consumed by the reducer
+  uint64_t* pfull_bar = oempty_bar + NSLOT;     // [NSLOT] predicted partials ready (4 checksum warps)
+  uint64_t* pempty_bar = pfull_bar + NSLOT;     // [NSLOT]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty_bar + NSLOT);
+  double* slot_obs = reinterpret_cast<double*>(tmem_slot + 4);  // [NSLOT][BM] (int64 bits for INT)
+  double* slot_pred = slot_obs + NSLOT * BM;                    // [NSLOT][BM]
+  uint32_t* bias_sm = reinterpret_cast<uint32_t*>(slot_pred + NSLOT * BM);  // [2][BN] bias of a tile
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int n_tiles = p.n_tiles;
+  const int m_pairs = (p.M + 2 * BM - 1) / (2 * BM);
+  // tiles t = t_first, t_first + t_step, ... < t_end: a contiguous range per pair (bands folded
+  // locally) or, when the concurrently streamed A bands would not fit in L2, a strided walk
+  const int pid = static_cast<int>(blockIdx.x >> 1), npairs = static_cast<int>(gridDim.x >> 1);
+  int t0, t1;
+  pair_range(pid, npairs, m_pairs * n_tiles, t0, t1);
+  const int t_first = p.sched ? pid : t0;
+  const int t_end = p.sched ? m_pairs * n_tiles : t1;
+  const int t_step = p.sched ? npairs : 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    if (p.c_tma) tma_prefetch(&tmC);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+      mbar_init(&aready_bar[s], 1);
+      mbar_init(&chkdone_bar[s], 4);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 8);
+    }
+    for (int b = 0; b < NSLOT; ++b) {
+      mbar_init(&ofull_bar[b], 4);
+      mbar_init(&oempty_bar[b], 1);
+      mbar_init(&pfull_bar[b], 4);
+      mbar_init(&pempty_bar[b], 1);
+    }
+    fence_barrier_init();
+    fence_proxy_async_smem();
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(tmem_slot, TMEM_COLS);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barrier inits and the TMEM allocation visible to both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // replay: a pair tile is recomputed when either of its two 128-row bands is active
+  auto pair_active = [&](int m) -> bool {
+    if (!p.replay) return true;
+    const int b0 = 2 * m, b1 = 2 * m + 1;
+    return (b0 < p.m_tiles && p.ws.band_active[b0]) || (b1 < p.m_tiles && p.ws.band_active[b1]);
+  };
+
+  if (warp == 0) {
+    // ================================================= TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);  // leader's barriers
+      int stage = 0;
+      uint32_t phase = 0, chk_pending = 0, chk_phase = 0;
+      for (int t = t_first; t < t_end; t += t_step) {
+        const int m = t / n_tiles, n = t - m * n_tiles;
+        if (!pair_active(m)) continue;
+        const int arow = m * 2 * BM + static_cast<int>(rank) * BM;
+        const int brow = n * BN + static_cast<int>(rank) * (BN / 2);
+        int rem = 0;  // kb % n_tiles
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          const bool mine = PROTECT && rem == n;
+          if (++rem == n_tiles) rem = 0;
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (chk_pending & (1u << stage)) {  // the checksum warps still hold the stage's previous K-block
+            mbar_wait(&chkdone_bar[stage], (chk_phase >> stage) & 1u);
+            chk_phase ^= 1u << stage;
+            chk_pending &= ~(1u << stage);
+          }
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (A_BYTES + B_BYTES));
+          const uint32_t fb = full0 + static_cast<uint32_t>(stage * 8);
+          tma_load_2d_pair(smA + stage * A_BYTES, &tmA, fb, kb * BK, arow);
+          tma_load_2d_pair(smB + stage * B_BYTES, &tmB, fb, kb * BK, brow);
+          if (mine) chk_pending |= 1u << stage;
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================= MMA issuer (leader)
+    if (rank == 0 && lane == 0) {
+      const uint32_t aready_peer = mapa_shared(smem_u32(&aready_bar[0]), 1);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = t_first; t < t_end; t += t_step) {
+        const int m = t / n_tiles, n = t - m * n_tiles;
+        if (!pair_active(m)) continue;
+        const int buf = local & 1;
+        GG_EV(10, local);
+        mbar_wait(&tempty_bar[buf], (static_cast<uint32_t>(local >> 1) & 1u) ^ 1u);
+        GG_EV(4, local);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+        int rem = 0;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          const bool mine = PROTECT && rem == n;
+          if (++rem == n_tiles) rem = 0;
+          mbar_wait(&full_bar[stage], phase);
+          if (mine) {  // both CTAs' halves of this stage have landed: let the checksum warps copy A
+            mbar_arrive(&aready_bar[stage]);
+            mbar_arrive_cluster(aready_peer + static_cast<uint32_t>(stage * 8));
+          }
+          tc_fence_after();
+          const uint64_t adesc = sw128_kmajor_desc(smem_u32(smA + stage * A_BYTES));
+          const uint64_t bdesc = sw128_kmajor_desc(smem_u32(smB + stage * B_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < MMAS_PER_STAGE; ++kk)
+            tc_mma_pair<T::MMA_KIND>(d_tmem, adesc + static_cast<uint64_t>(kk * (MMA_K_BYTES >> 4)),
+                                     bdesc + static_cast<uint64_t>(kk * (MMA_K_BYTES >> 4)), IDESC,
+                                     (kb | kk) != 0 ? 1u : 0u);
+          tc_commit_pair(&empty_bar[stage], 0x3);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_pair(&tfull_bar[buf], 0x3);
+        GG_EV(5, local);
+        ++local;
+      }
+    }
+  } else if (warp == 3) {
+    // ================================================= reducer
+    if constexpr (PROTECT) {
+      double of[4] = {0.0, 0.0, 0.0, 0.0}, pf[4] = {0.0, 0.0, 0.0, 0.0};
+      long long oi[4] = {0, 0, 0, 0}, pi[4] = {0, 0, 0, 0};
+      int local = 0;
+      for (int t = t_first; t < t_end; t += t_step) {
+        const int m = t / n_tiles, n = t - m * n_tiles;
+        if (!pair_active(m)) continue;
+        const int slot = local % NSLOT;
+        const uint32_t ph = static_cast<uint32_t>(local / NSLOT) & 1u;
+        if (lane == 0) GG_EV(11, local);
+        mbar_wait(&ofull_bar[slot], ph);
+        if (lane == 0) GG_EV(12, local);
+        mbar_wait(&pfull_bar[slot], ph);
+        if (lane == 0) GG_EV(8, local);
+        const int mb = 2 * m + static_cast<int>(rank);
+        const bool band_ok = mb < p.m_tiles && (!p.replay || p.ws.band_active[mb]) && !(p.dbg & 4);
+        const bool whole = !p.sched && (m * n_tiles >= t0) && ((m + 1) * n_tiles <= t1);  // band folded locally
+        if (band_ok) {
+          if (whole) {
+            if (n == 0) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) { of[q] = 0.0; pf[q] = 0.0; oi[q] = 0; pi[q] = 0; }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // ascending-tile fold, identical to the split-band fold
+              const int i = slot * BM + lane + 32 * q;
+              if constexpr (INT) {
+                oi[q] += reinterpret_cast<const long long*>(slot_obs)[i];
+                pi[q] += reinterpret_cast<const long long*>(slot_pred)[i];
+              } else {
+                of[q] += slot_obs[i];
+                pf[q] += slot_pred[i];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int i = lane + 32 * q;
+              const size_t g = static_cast<size_t>(n) * p.m_pad + mb * BM + i;
+              p.ws.partial[g] = slot_obs[slot * BM + i];
+              p.ws.pred[g] = slot_pred[slot * BM + i];
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&oempty_bar[slot]);
+          mbar_arrive(&pempty_bar[slot]);
+        }
+        if (band_ok) {
+          if (whole) {
+            if (n == n_tiles - 1) finish_band<INT>(p, mb, lane, of, pf, oi, pi);
+          } else {
+            __threadfence();  // release this tile's partials
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) {
+              last = (atomicAdd(&p.ws.band_counter[mb], 1) == n_tiles - 1) ? 1 : 0;
+              if (last) {
+                __threadfence();  // acquire the other pairs' partials
+                p.ws.band_counter[mb] = 0;
+              }
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+              double sof[4] = {0.0, 0.0, 0.0, 0.0}, spf[4] = {0.0, 0.0, 0.0, 0.0};
+              long long soi[4] = {0, 0, 0, 0}, spi[4] = {0, 0, 0, 0};
+              for (int tt = 0; tt < n_tiles; ++tt) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const size_t g = static_cast<size_t>(tt) * p.m_pad + mb * BM + lane + 32 * q;
+                  if constexpr (INT) {
+                    soi[q] += ldcg_i64(reinterpret_cast<const long long*>(p.ws.partial) + g);
+                    spi[q] += ldcg_i64(reinterpret_cast<const long long*>(p.ws.pred) + g);
+                  } else {
+                    sof[q] += ldcg_f64(p.ws.partial + g);
+                    spf[q] += ldcg_f64(p.ws.pred + g);
+                  }
+                }
+              }
+              finish_band<INT>(p, mb, lane, sof, spf, soi, spi);
+            }
+          }
+        }
+        if (lane == 0) GG_EV(9, local);
+        ++local;
+      }
+    }
+  } else if (warp >= 8) {
+    // ================================================= epilogue (highest warp ids: the SMSP
+    // arbiter issues highest-id-first, so the critical-path warps win every tie)
+    const int eg = warp - 8;            // TMEM lane group (warp % 4) / 32-row slab of this CTA
+    const int tid = threadIdx.x - 256;  // accumulator row within this CTA's 128
+    const bool c_tma = p.c_tma != 0 && !p.replay;
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    int cbuf = 0;
+    int local = 0;
+    for (int t = t_first; t < t_end; t += t_step) {
+      const int m = t / n_tiles, n = t - m * n_tiles;
+      if (!pair_active(m)) continue;
+      const int buf = local & 1;
+      const uint32_t use = static_cast<uint32_t>(local >> 1);
+      // this tile's 256 bias values into shared memory (broadcast reads below; no reliance on L1)
+      {
+        uint32_t* bsm = bias_sm + buf * BN;
+        const int c = n * BN + 2 * tid;
+        const uint32_t* bg = static_cast<const uint32_t*>(p.bias);
+        bsm[2 * tid] = (bg != nullptr && c < p.N) ? __ldg(bg + c) : 0u;
+        bsm[2 * tid + 1] = (bg != nullptr && c + 1 < p.N) ? __ldg(bg + c + 1) : 0u;
+        named_bar_sync(1, 128);
+      }
+      mbar_wait(&tfull_bar[buf], use & 1);
+      if (tid == 0) GG_EV(0, local);
+      tc_fence_after();
+      const int row0 = m * 2 * BM + static_cast<int>(rank) * BM;
+      const int row = row0 + tid;
+      const bool row_ok = row < p.M;
+      const int n0 = n * BN;
+      const int nchunks = min(BN / 32, (p.N - n0 + 31) / 32);
+      double obs = 0.0;
+      float obs4[4] = {0.f, 0.f, 0.f, 0.f};  // 16-bit outputs: per-tile fp32 chains
+      long long obs_i = 0;
+      int changed = 0;
+#ifdef GG_TRACE
+      long long tr_ld = 0, tr_cmp = 0, tr_st = 0, tr_obs = 0, tr_t = clock64();
+#define GG_LAP(acc)                 \
+  do {                              \
+    const long long now = clock64(); \
+    acc += now - tr_t;              \
+    tr_t = now;                     \
+  } while (0)
+#else
+#define GG_LAP(acc) \
+  do {              \
+  } while (0)
+#endif
+#pragma unroll 1
+      for (int c = 0; c < nchunks; ++c) {
+        const int col0 = n0 + 32 * c;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(
+            tmem_base + (static_cast<uint32_t>(eg * 32) << 16) + static_cast<uint32_t>(buf * BN + 32 * c), r);
+        tmem_ld_wait();
+        GG_LAP(tr_ld);
+        if (c == nchunks - 1) {  // TMEM buffer drained: hand it back to the leader's MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty0 + static_cast<uint32_t>(buf * 8));
+          if (tid == 0) GG_EV(1, local);
+        }
+        const bool full = (col0 + 32 <= p.N);
+        bool out_inj = false;  // an output fault lands in this row's chunk (rare)
+        for (int i = 0; i < p.n_inj; ++i) {
+          const gg_injection f = p.inj[i];
+          if (f.row == row && f.col >= col0 && f.col < col0 + 32) {
+            if (f.target == GG_INJ_ACCUMULATOR) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)  // static indices keep r[] in registers
+                if (f.col == col0 + j) r[j] ^= (1u << (f.bit & 31));
+            } else {
+              out_inj = true;
+            }
+          }
+        }
+        // bias (fp32 bits, or int32) of the 32 columns, from the tile's smem copy
+        uint32_t bb[32];
+        {
+          const uint32_t baddr = smem_u32(bias_sm + buf * BN + 32 * c);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint4 bv = lds128(baddr + 16 * q);
+            bb[4 * q] = bv.x; bb[4 * q + 1] = bv.y; bb[4 * q + 2] = bv.z; bb[4 * q + 3] = bv.w;
+          }
+        }
+        // o[] holds the stored encodings: packed 16-bit pairs in o[0..15] for bf16/fp16
+        // outputs (element 2i in the low half), one 32-bit encoding per column otherwise
+        uint32_t o[32];
+        if constexpr (OUT16) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float lo = __uint_as_float(r[2 * i]) + __uint_as_float(bb[2 * i]);
+            const float hi = __uint_as_float(r[2 * i + 1]) + __uint_as_float(bb[2 * i + 1]);
+            o[i] = (OUT == O_BF16) ? pack_bf16x2(lo, hi) : pack_f16x2(lo, hi);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = acc_to_out_bits<OUT>(r[j], bb[j]);
+        }
+        if (out_inj) {
+          for (int i = 0; i < p.n_inj; ++i) {
+            const gg_injection f = p.inj[i];
+            if (f.row != row || f.target != GG_INJ_OUTPUT || f.col < col0 || f.col >= col0 + 32) continue;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {  // static indices keep o[] in registers
+              if (f.col != col0 + j) continue;
+              if constexpr (OUT16) {
+                const int sh = 16 * (j & 1);
+                const uint32_t old = (o[j >> 1] >> sh) & 0xFFFFu;
+                const uint32_t nw = (f.mode == GG_INJ_BITFLIP) ? ((old ^ (1u << (f.bit & 31))) & 0xFFFFu)
+                                                               : value_to_out_bits<OUT>(f.value);
+                o[j >> 1] = (o[j >> 1] & ~(0xFFFFu << sh)) | (nw << sh);
+              } else {
+                o[j] = (f.mode == GG_INJ_BITFLIP) ? (o[j] ^ (1u << (f.bit & 31))) : value_to_out_bits<OUT>(f.value);
+              }
+            }
+          }
+        }
+        GG_LAP(tr_cmp);
+        if constexpr (PROTECT) {  // observed row sum of the STORED values (guard.py:170)
+          if (row_ok) {
+            if constexpr (INT) {
+              long long s = 0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (full || col0 + j < p.N) s += static_cast<long long>(static_cast<int>(o[j]));
+              obs_i += s;
+            } else if constexpr (OUT == O_F32) {
+              double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (full || col0 + j < p.N) s4[j & 3] += static_cast<double>(__uint_as_float(o[j]));
+              obs += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            } else {
+              // 16-bit outputs are exact in fp32: four fp32 chains over the tile's 256 columns
+              // (error <= 64 * 2^-24 of the chain magnitude, far below the output rounding),
+              // folded into fp64 once per tile
+              if (full) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  float xl, xh;
+                  if constexpr (OUT == O_BF16) {
+                    xl = __uint_as_float(o[i] << 16);
+                    xh = __uint_as_float(o[i] & 0xFFFF0000u);
+                  } else {
+                    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&o[i]));
+                    xl = f.x;
+                    xh = f.y;
+                  }
+                  obs4[(2 * i) & 3] += xl;
+                  obs4[(2 * i + 1) & 3] += xh;
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  const uint32_t h = (o[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+                  if (col0 + j < p.N) obs4[j & 3] += (OUT == O_BF16) ? bf16_bits_to_f32(h) : f16_bits_to_f32(h);
+                }
+              }
+            }
+          }
+        }
+        GG_LAP(tr_obs);
+        if (c_tma) {
+          // coalesced store: this warp's 32 rows x 32 columns through a swizzled smem box + TMA
+          uint8_t* boxp = smC + (eg * 2 + cbuf) * CST_BYTES;
+          if (lane == 0) bulk_wait_read<1>();  // the box written two chunks ago has been read
+          __syncwarp();
+          stage_row<OUT>(smem_u32(boxp), lane, o);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, boxp, col0, row0 + 32 * eg);
+            bulk_commit();
+          }
+          cbuf ^= 1;
+          GG_LAP(tr_st);
+        } else if (row_ok) {
+          const long long base = static_cast<long long>(row) * p.ldc + col0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (col0 + j >= p.N) continue;
+            const uint32_t e = OUT16 ? ((o[j >> 1] >> (16 * (j & 1))) & 0xFFFFu) : o[j];
+            if (p.replay) changed += (load_out_bits<OUT>(p.C, base + j) != e) ? 1 : 0;
+            store_out_bits<OUT>(p.C, base + j, e);
+          }
+        }
+      }
+      if (nchunks <= 0) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty0 + static_cast<uint32_t>(buf * 8));
+      }
+      if (p.replay && p.changed != nullptr) {
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o2);
+        if (lane == 0 && changed) atomicAdd(p.changed, changed);
+      }
+      if constexpr (OUT16) obs += (static_cast<double>(obs4[0]) + static_cast<double>(obs4[1])) +
+                                 (static_cast<double>(obs4[2]) + static_cast<double>(obs4[3]));
+      if (tid == 0) GG_EV(2, local);
+#ifdef GG_TRACE
+      if (tid == 0 && g_trace != nullptr && local < TRACE_TILES) {
+        const size_t b = (static_cast<size_t>(blockIdx.x) * TRACE_TILES + local) * TRACE_EV;
+        g_trace[b + 13] = tr_ld;
+        g_trace[b + 14] = tr_cmp;
+        g_trace[b + 15] = tr_st;
+        g_trace[b + 16] = tr_obs;
+      }
+#endif
+      if constexpr (PROTECT) {
+        const int slot = local % NSLOT;
+        mbar_wait(&oempty_bar[slot], (static_cast<uint32_t>(local / NSLOT) & 1u) ^ 1u);
+        if (tid == 0) GG_EV(3, local);
+        if constexpr (INT) reinterpret_cast<long long*>(slot_obs)[slot * BM + tid] = obs_i;
+        else slot_obs[slot * BM + tid] = obs;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ofull_bar[slot]);
+      }
+      ++local;
+    }
+    if (c_tma && lane == 0) bulk_wait_all();
+  } else if (warp >= 4 && warp < 8) {
+    // ================================================= checksum producer side
+    if constexpr (PROTECT) {
+      const int tid = threadIdx.x - 128;  // row within this CTA's 128
+      const int sw = tid & 7;             // 128B-swizzle phase of this row
+      int stage = 0;
+      uint32_t ar_phase = 0;
+      int local = 0;
+      for (int t = t_first; t < t_end; t += t_step) {
+        const int m = t / n_tiles, n = t - m * n_tiles;
+        if (!pair_active(m)) continue;
+        double accd = 0.0;
+        long long acci = 0;
+        int rem = 0;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          const int s = stage;
+          if (++stage == STAGES) stage = 0;
+          const bool mine = (rem == n);
+          if (++rem == n_tiles) rem = 0;
+          if (!mine) continue;  // this tile's share of the band: K-blocks kb == n (mod n_tiles)
+          mbar_wait(&aready_bar[s], (ar_phase >> s) & 1u);
+          ar_phase ^= 1u << s;
+          uint4 v[8];  // this row's 128 B of the stage (16-byte chunk j holds K-bytes 16j..16j+15)
+          const uint32_t rowaddr = smem_u32(smA + s * A_BYTES) + static_cast<uint32_t>(tid * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = lds128(rowaddr + static_cast<uint32_t>((j ^ sw) << 4));
+          fence_proxy_async_smem();  // generic reads of the stage before its TMA refill
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&chkdone_bar[s]);
+          // w-vectors are zero-padded to whole K-blocks (gg_checksum_aux) and TMA zero-fills
+          // x beyond K: no tail checks.  Independent accumulators for ILP.
+          if constexpr (INT) {
+            // sum_k x*w = sum_d 256^d sum_k x*digit_d(w): exact IDP4A over 128 K per block
+            const int4* dig = static_cast<const int4*>(p.w_aux) + kb * (BK / 4);
+            int a[2][3] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int4 dd = __ldg(dig + j * 4 + q);
+                a[q & 1][0] = __dp4a(static_cast<int>(w4[q]), dd.x, a[q & 1][0]);
+                a[q & 1][1] = __dp4a(static_cast<int>(w4[q]), dd.y, a[q & 1][1]);
+                a[q & 1][2] = __dp4a(static_cast<int>(w4[q]), dd.z, a[q & 1][2]);
+              }
+            }
+            acci += static_cast<long long>(a[0][0] + a[1][0]) + 256ll * (a[0][1] + a[1][1]) +
+                    65536ll * (a[0][2] + a[1][2]);
+          } else if constexpr (KIND == K_TF32) {
+            const double2* wd = reinterpret_cast<const double2*>(static_cast<const double*>(p.w_aux) + kb * BK);
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const double2 w01 = __ldg(wd + 2 * j), w23 = __ldg(wd + 2 * j + 1);
+              a[0] = fma(static_cast<double>(__uint_as_float(v[j].x)), w01.x, a[0]);
+              a[1] = fma(static_cast<double>(__uint_as_float(v[j].y)), w01.y, a[1]);
+              a[2] = fma(static_cast<double>(__uint_as_float(v[j].z)), w23.x, a[2]);
+              a[3] = fma(static_cast<double>(__uint_as_float(v[j].w)), w23.y, a[3]);
+            }
+            accd += (a[0] + a[1]) + (a[2] + a[3]);
+          } else {
+            // bf16/fp16 x is exact in fp32; w = fp32(w_sum) (|w - w_sum| <= 2^-24 |w_sum|).
+            const float4* wq = reinterpret_cast<const float4*>(static_cast<const float*>(p.w_aux) + kb * BK);
+            float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 wa = __ldg(wq + 2 * j), wb = __ldg(wq + 2 * j + 1);
+              float x[8];
+              const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if constexpr (KIND == K_BF16) {
+                  x[2 * q] = __uint_as_float(w4[q] << 16);
+                  x[2 * q + 1] = __uint_as_float(w4[q] & 0xFFFF0000u);
+                } else {
+                  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[q]));
+                  x[2 * q] = f.x;
+                  x[2 * q + 1] = f.y;
+                }
+              }
+              a[0] = fmaf(x[0], wa.x, a[0]);
+              a[1] = fmaf(x[1], wa.y, a[1]);
+              a[2] = fmaf(x[2], wa.z, a[2]);
+              a[3] = fmaf(x[3], wa.w, a[3]);
+              a[0] = fmaf(x[4], wb.x, a[0]);
+              a[1] = fmaf(x[5], wb.y, a[1]);
+              a[2] = fmaf(x[6], wb.z, a[2]);
+              a[3] = fmaf(x[7], wb.w, a[3]);
+            }
+            accd += (static_cast<double>(a[0]) + static_cast<double>(a[1])) +
+                    (static_cast<double>(a[2]) + static_cast<double>(a[3]));
+          }
+        }
+        if (tid == 0) GG_EV(6, local);
+        const int slot = local % NSLOT;
+        mbar_wait(&pempty_bar[slot], (static_cast<uint32_t>(local / NSLOT) & 1u) ^ 1u);
+        if (tid == 0) GG_EV(7, local);
+        if constexpr (INT) reinterpret_cast<long long*>(slot_pred)[slot * BM + tid] = acci;
+        else slot_pred[slot * BM + tid] = accd;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull_bar[slot]);
+        ++local;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's smem / barriers / TMEM stay alive until both CTAs are done
+  if (warp == 2) tmem_dealloc_pair(tmem_base, TMEM_COLS);
+}
+
+}  // namespace pair
+}  // namespace gg

@@ -4,10 +4,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
-#include "gg_gemm_sm100.cuh"
+#include "gg_gemm2_sm100.cuh"
 #include "gg_internal.h"
 
 namespace gg {
@@ -34,12 +36,29 @@ int make_operand_map(CUtensorMap* map, CUtensorMapDataType dt, int elem, const v
   if (enc == nullptr) return fail(GG_ECUDA, "cuTensorMapEncodeTiled is unavailable (driver too old?)");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_bytes)};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK_BYTES / elem), box_rows};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(pair::BK_BYTES / elem), box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(GG_ECUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string(int(r)) + ")");
+  return 0;
+}
+
+// Output map for the TMA-store epilogue: [M, N] row-major with pitch ld_bytes,
+// box = 32 columns x 32 rows, swizzle matching the epilogue's smem staging.
+int make_output_map(CUtensorMap* map, CUtensorMapDataType dt, int elem, void* ptr, int64_t N, int64_t M,
+                    int64_t ld_bytes) {
+  auto enc = tensor_map_encoder();
+  if (enc == nullptr) return fail(GG_ECUDA, "cuTensorMapEncodeTiled is unavailable (driver too old?)");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_bytes)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(pair::CBOX), static_cast<cuuint32_t>(pair::CBOX)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, dt, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   elem == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(GG_ECUDA, "cuTensorMapEncodeTiled (C) failed (code " + std::to_string(int(r)) + ")");
   return 0;
 }
 
@@ -100,23 +119,24 @@ __global__ void replay_prepare_kernel(const uint8_t* rows, int M, int m_tiles, u
 }
 
 template <int KIND, int OUT, bool PROTECT>
-int launch_instance(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid, cudaStream_t s) {
-  auto kern = gg_protected_gemm_kernel<KIND, OUT, PROTECT>;
+int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p, int grid,
+                         cudaStream_t s) {
+  auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT>;
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
-      return fail(GG_ECUDA, "cudaFuncSetAttribute(max dynamic smem) failed");
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES) != cudaSuccess)
+      return fail(GG_ECUDA, "cudaFuncSetAttribute(max dynamic smem, pair kernel) failed");
     configured = true;
   }
-  kern<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, p);
-  return check_launch("protected_gemm");
+  kern<<<grid, pair::THREADS, pair::SMEM_BYTES, s>>>(ta, tb, tc, p);
+  return check_launch("protected_gemm_pair");
 }
 
 template <int KIND, int OUT>
-int dispatch_protect(bool protect, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, int grid,
-                     cudaStream_t s) {
-  return protect ? launch_instance<KIND, OUT, true>(ta, tb, p, grid, s)
-                 : launch_instance<KIND, OUT, false>(ta, tb, p, grid, s);
+int dispatch_protect(bool protect, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
+                     int grid, cudaStream_t s) {
+  return protect ? launch_pair_instance<KIND, OUT, true>(ta, tb, tc, p, grid, s)
+                 : launch_pair_instance<KIND, OUT, false>(ta, tb, tc, p, grid, s);
 }
 
 }  // namespace
@@ -162,8 +182,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
     if (!int_kind && d->chk_prec != GG_P_F64)
       return fail(GG_EUNSUPPORTED, "fused checksum supports binary64 precision for float kinds (use gg_verify_rows)");
     if (reinterpret_cast<uintptr_t>(d->w_sum) & 15) return fail(GG_EINVAL, "protected_gemm: w_sum must be 16-byte aligned");
-    if ((kind == K_BF16 || kind == K_F16 || kind == K_I8) &&
-        (d->w_aux == nullptr || (reinterpret_cast<uintptr_t>(d->w_aux) & 15)))
+    if (d->w_aux == nullptr || (reinterpret_cast<uintptr_t>(d->w_aux) & 15))
       return fail(GG_EINVAL, "protected_gemm: w_aux (gg_checksum_aux) is required and must be 16-byte aligned");
     if (!d->w_sum || !d->d || !d->flags || !d->max_disc || !d->nflag || !d->triggered)
       return fail(GG_EINVAL, "protected_gemm: protect=1 needs w_sum, d, flags, max_disc, nflag, triggered");
@@ -181,8 +200,18 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   CUtensorMap ta, tb;
   int rc = make_operand_map(&ta, tdt, elem, d->A, d->K, d->M, d->lda * elem, BM);
   if (rc) return rc;
-  rc = make_operand_map(&tb, tdt, elem, d->B, d->K, d->N, d->ldb * elem, BN);
+  rc = make_operand_map(&tb, tdt, elem, d->B, d->K, d->N, d->ldb * elem, pair::BN / 2);
   if (rc) return rc;
+  // C through the TMA-store epilogue when the pointer and pitch allow it
+  const int out_elem = (out == O_BF16 || out == O_F16) ? 2 : 4;
+  const CUtensorMapDataType cdt = out == O_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                  : out == O_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                  : out == O_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                 : CU_TENSOR_MAP_DATA_TYPE_INT32;
+  CUtensorMap tc;
+  std::memset(&tc, 0, sizeof(tc));
+  int c_tma = ((reinterpret_cast<uintptr_t>(d->C) & 15) == 0 && (d->ldc * out_elem) % 16 == 0) ? 1 : 0;
+  if (c_tma && make_output_map(&tc, cdt, out_elem, d->C, d->N, d->M, d->ldc * out_elem) != 0) c_tma = 0;
 
   Params p{};
   p.M = static_cast<int>(d->M);
@@ -190,10 +219,20 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.K = static_cast<int>(d->K);
   p.m_tiles = static_cast<int>((d->M + BM - 1) / BM);
   p.n_tiles = static_cast<int>((d->N + BN - 1) / BN);
-  p.k_blocks = static_cast<int>((d->K * elem + BK_BYTES - 1) / BK_BYTES);
+  p.k_blocks = static_cast<int>((d->K * elem + pair::BK_BYTES - 1) / pair::BK_BYTES);
   p.m_pad = p.m_tiles * BM;
+  p.A = d->A;
+  p.lda = d->lda;
   p.C = d->C;
   p.ldc = d->ldc;
+  p.c_tma = c_tma;
+  {
+    static const int dbg = [] {
+      const char* e = std::getenv("GG_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    p.dbg = dbg;
+  }
   p.bias = d->bias;
   p.w_sum = d->w_sum;
   p.w_aux = d->w_aux;
@@ -211,6 +250,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.inj = d->inj;
   p.n_inj = d->n_inj;
   p.replay = replay ? 1 : 0;
+
   p.changed = d->changed;
   if (protect) {
     const WsLayout L = ws_layout(d->M, d->N);
@@ -229,21 +269,32 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
     rc = check_launch("replay_prepare");
     if (rc) return rc;
   }
-  const int tiles = p.m_tiles * p.n_tiles;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int pair_tiles = ((p.M + 2 * pair::BM - 1) / (2 * pair::BM)) * p.n_tiles;
+  const int pairs = pair_tiles < num_sms() / 2 ? pair_tiles : num_sms() / 2;
+  const int grid = 2 * pairs;
+  // A bands streamed concurrently by all pairs (256 rows x K each): keep them L2-resident
+  const double a_footprint = static_cast<double>(pairs) * 2 * pair::BM * static_cast<double>(d->K) * elem;
+  p.sched = a_footprint > 40.0e6 ? 1 : 0;
 
   switch (kind) {
     case K_BF16:
-      return out == O_BF16 ? dispatch_protect<K_BF16, O_BF16>(protect, ta, tb, p, grid, s)
-                           : dispatch_protect<K_BF16, O_F32>(protect, ta, tb, p, grid, s);
+      return out == O_BF16 ? dispatch_protect<K_BF16, O_BF16>(protect, ta, tb, tc, p, grid, s)
+                           : dispatch_protect<K_BF16, O_F32>(protect, ta, tb, tc, p, grid, s);
     case K_F16:
-      return out == O_F16 ? dispatch_protect<K_F16, O_F16>(protect, ta, tb, p, grid, s)
-                          : dispatch_protect<K_F16, O_F32>(protect, ta, tb, p, grid, s);
+      return out == O_F16 ? dispatch_protect<K_F16, O_F16>(protect, ta, tb, tc, p, grid, s)
+                          : dispatch_protect<K_F16, O_F32>(protect, ta, tb, tc, p, grid, s);
     case K_TF32:
-      return dispatch_protect<K_TF32, O_F32>(protect, ta, tb, p, grid, s);
+      return dispatch_protect<K_TF32, O_F32>(protect, ta, tb, tc, p, grid, s);
     default:
-      return dispatch_protect<K_I8, O_I32>(protect, ta, tb, p, grid, s);
+      return dispatch_protect<K_I8, O_I32>(protect, ta, tb, tc, p, grid, s);
   }
 }
+
+#ifdef GG_TRACE
+extern "C" __attribute__((visibility("default"))) int gg_trace_buffer(void* buf) {
+  unsigned long long* b = static_cast<unsigned long long*>(buf);
+  return cudaMemcpyToSymbol(pair::g_trace, &b, sizeof(b)) == cudaSuccess ? 0 : GG_ECUDA;
+}
+#endif
 
 }  // namespace gg

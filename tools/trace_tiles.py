@@ -1,0 +1,56 @@
+"""Per-tile role timeline of one protected GEMM from the GG_TRACE library.
+
+    GEMMGUARD_LIB=paper_2310_03841_b200/_build/libgemmguard_b200_trace.so \
+        python tools/trace_tiles.py M N K [protect]
+"""
+import ctypes, os, sys
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+from paper_2310_03841_b200 import kernels as K, _lib as L
+M, N, Kd = [int(v) for v in sys.argv[1:4]]
+protect = (sys.argv[4] != '0') if len(sys.argv) > 4 else True
+x = torch.randn(M, Kd, device='cuda').to(torch.bfloat16); w = (torch.randn(N, Kd, device='cuda') / Kd**.5).to(torch.bfloat16)
+b = torch.zeros(N, device='cuda')
+ws, bs = K.offline_checksum(w, b, L.GG_P_F64); aux = K.checksum_aux(ws, torch.bfloat16); bsv = bs.item()
+y = torch.empty(M, N, dtype=torch.bfloat16, device='cuda'); res = K.CheckResult.empty(M, False, 'cuda')
+lib = L.load(); lib.gg_trace_buffer.argtypes = [ctypes.c_void_p]
+TT, EV = 64, 20
+buf = torch.zeros(148 * TT * EV, dtype=torch.int64, device='cuda')
+run = (lambda: K.protected_gemm(x, w, b, w_sum=ws, w_aux=aux, bias_sum=bsv, lo=-1e30, hi=1e30, out=y, result=res)) \
+    if protect else (lambda: K.protected_gemm(x, w, b, protect=False, out=y))
+for _ in range(3): run()
+torch.cuda.synchronize()
+lib.gg_trace_buffer(ctypes.c_void_p(buf.data_ptr()))
+run(); torch.cuda.synchronize()
+lib.gg_trace_buffer(ctypes.c_void_p(0))
+t = buf.view(148, TT, EV).cpu().numpy().astype(np.int64)
+names = {0: 'epi_tfull', 1: 'epi_tmem_rel', 2: 'epi_done', 3: 'epi_slot', 4: 'mma_start', 5: 'mma_end',
+         6: 'chk_done', 7: 'chk_slot', 8: 'red_got', 9: 'red_done', 10: 'mma_wait_tempty', 11: 'red_wait', 12: 'red_obs'}
+def stats(cta):
+    r = t[cta]; n = int((r[:, 4] > 0).sum()) if cta % 2 == 0 else int((r[:, 0] > 0).sum())
+    return r, n
+for cta in (0, 1, 40, 41):
+    r, n = stats(cta)
+    base = r[r > 0].min() if (r > 0).any() else 0
+    print(f'--- CTA {cta}: tiles {n}')
+    for i in range(min(n, 12)):
+        row = r[i]
+        f = lambda e: (row[e] - base) if row[e] > 0 else -1
+        print(f' tile {i:2d}: mma wait {f(10):8d} start {f(4):8d} end {f(5):8d} | epi tfull {f(0):8d} rel {f(1):8d} done {f(2):8d} slot {f(3):8d}'
+              f' | chk done {f(6):8d} slot {f(7):8d} | red wait {f(11):8d} obs {f(12):8d} got {f(8):8d} done {f(9):8d}')
+# aggregate over leader CTAs: mma issue time vs epilogue time per tile
+mma, epi, gapt = [], [], []
+for cta in range(0, 148, 2):
+    r, n = stats(cta)
+    for i in range(1, min(n, TT)):
+        if r[i, 4] and r[i, 5]: mma.append(r[i, 5] - r[i, 4])
+        if r[i, 0] and r[i, 2]: epi.append(r[i, 2] - r[i, 0])
+        if r[i, 4] and r[i, 10]: gapt.append(r[i, 4] - r[i, 10])
+ld = [t[c, i, 13] for c in range(148) for i in range(TT) if t[c, i, 0] > 0]
+cp = [t[c, i, 14] for c in range(148) for i in range(TT) if t[c, i, 0] > 0]
+st = [t[c, i, 15] for c in range(148) for i in range(TT) if t[c, i, 0] > 0]
+ob = [t[c, i, 16] for c in range(148) for i in range(TT) if t[c, i, 0] > 0]
+print('epilogue per tile (median cycles): tmem load+wait', np.median(ld), 'convert', np.median(cp), 'obs', np.median(ob), 'stage+tma', np.median(st))
+print('median cycles: mma issue', np.median(mma) if mma else None, 'epilogue', np.median(epi) if epi else None,
+      'mma wait tempty', np.median(gapt) if gapt else None)
