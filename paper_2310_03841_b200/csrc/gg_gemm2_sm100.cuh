@@ -18,7 +18,7 @@
 // instead (neighbouring pairs share A bands in L2) and every band exchanges
 // its partials through global memory.
 //
-// Warp roles (384 threads per CTA):
+// Warp roles (512 threads per CTA):
 //   0      TMA producer (both CTAs; loads complete on the LEADER's full barrier)
 //   1      MMA issuer (leader only, one thread): stage release and
 //          accumulator hand-off are tcgen05.commit multicasts to both CTAs.
@@ -26,18 +26,18 @@
 //   3      reducer: folds the per-tile row partials of each band (registers
 //          for local bands, global partials + one fence for split bands),
 //          writes d / flags and the launch summaries
-//   8-11   epilogue: TMEM -> registers, bias, round, fault injection,
+//   4-11   epilogue, two warps per TMEM lane quadrant (each owns half of the
+//          tile's columns): TMEM -> registers, bias, round, fault injection,
 //          OBSERVED row sums over the stored values (guard.py:170), then a
 //          32x32 swizzled smem box per warp and a TMA store (coalesced C).
-//          Highest warp ids: the SMSP arbiter issues highest-id-first, so the
-//          critical-path warps win every issue tie.
-//   4-7    checksum producer side: PREDICTED[m] = A[m,:] . w_sum (guard.py:
-//          168-169) from the A stages already in shared memory.  A band's
-//          K-blocks are dealt round-robin over its N-tiles; the MMA thread
-//          relays "owned stage landed" (local + remote mbarrier arrive) before
-//          issuing that stage's MMAs, the checksum warps copy their row to
-//          registers at once and release the stage, so the refill of an owned
-//          stage is not delayed.
+//   12-15  checksum producer side: PREDICTED[m] = A[m,:] . w_sum (guard.py:
+//          168-169) from the A stages already in shared memory, w from shared
+//          memory.  A band's K-blocks are dealt round-robin over its N-tiles;
+//          the MMA thread relays "owned stage landed" (local + remote arrive)
+//          before issuing that stage's MMAs, the checksum warps copy their row
+//          to registers and release the stage at once.  Highest warp ids: the
+//          SMSP arbiter issues highest-id-first, and the producer waits on these
+//          bursty warps before refilling an owned stage.
 // Everything is deterministic (fixed fold orders, no float atomics), so a
 // recompute is byte-identical — required by replay (guard.py:590).
 #pragma once
@@ -50,7 +50,7 @@ namespace pair {
 // device buffer (gg_trace_buffer); compiled out of the production library.
 #ifdef GG_TRACE
 __device__ unsigned long long* g_trace = nullptr;
-constexpr int TRACE_TILES = 64, TRACE_EV = 20;
+constexpr int TRACE_TILES = 64, TRACE_EV = 24;
 #define GG_EV(ev, local)                                                                                  \
   do {                                                                                                  \
     if (g_trace != nullptr && (local) < TRACE_TILES)                                                    \
@@ -66,18 +66,20 @@ constexpr int BM = 128;           // rows per CTA (256 per pair)
 constexpr int BN = 256;           // MMA N per tile; each CTA stages BN/2 rows of B
 constexpr int BK_BYTES = 128;     // one 128 B swizzle atom of K per stage
 constexpr int STAGES = 5;
-constexpr int THREADS = 384;
+constexpr int THREADS = 512;
 constexpr int A_BYTES = BM * BK_BYTES;        // 16 KB
 constexpr int B_BYTES = (BN / 2) * BK_BYTES;  // 16 KB
 constexpr int TMEM_COLS = 2 * BN;
-constexpr int CBOX = 32;                      // epilogue store box: 32 rows x 32 columns per warp
-constexpr int CST_BYTES = CBOX * CBOX * 4;    // 4 KB staging per box (2 KB used by 16-bit outputs)
+constexpr int EPI_WARPS = 8;                 // two per TMEM lane quadrant, each owning half the columns
+constexpr int CBOX = 32;                      // epilogue store box: 32 rows x 32 columns
+constexpr int CST_BYTES = 4096;               // staging per epilogue warp: 2 x 2 KB boxes (16-bit out) or 1 x 4 KB
 constexpr int C_OFF = STAGES * (A_BYTES + B_BYTES);
-constexpr int BAR_OFF = C_OFF + 4 * 2 * CST_BYTES;
+constexpr int BAR_OFF = C_OFF + EPI_WARPS * CST_BYTES;
 constexpr int NSLOT = 4;                      // depth of the observed / predicted partial rings
 constexpr int NBAR = 4 * STAGES + 4 + 4 * NSLOT;
-constexpr int SMEM_BYTES = BAR_OFF + NBAR * 8 + 16 /*tmem slot*/ + 2 * NSLOT * BM * 8 /*partial rings*/ +
-                           2 * BN * 4 /*bias tiles*/ + 1024 /*align*/;
+constexpr int W_SMEM = 16384;                 // checksum w-vector kept in shared memory when it fits
+constexpr int SMEM_BYTES = BAR_OFF + NBAR * 8 + 16 /*tmem slot*/ + 3 * NSLOT * BM * 8 /*partial rings*/ +
+                           2 * BN * 4 /*bias tiles*/ + W_SMEM + 1024 /*align*/;
 
 template <int KIND> struct PairIdesc;
 template <> struct PairIdesc<K_BF16> { static constexpr uint32_t V = make_idesc(1, 1, 256, BN); };
@@ -223,9 +225,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* pfull_bar = oempty_bar + NSLOT;     // [NSLOT] predicted partials ready (4 checksum warps)
   uint64_t* pempty_bar = pfull_bar + NSLOT;     // [NSLOT]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty_bar + NSLOT);
-  double* slot_obs = reinterpret_cast<double*>(tmem_slot + 4);  // [NSLOT][BM] (int64 bits for INT)
-  double* slot_pred = slot_obs + NSLOT * BM;                    // [NSLOT][BM]
+  double* slot_obs = reinterpret_cast<double*>(tmem_slot + 4);  // [NSLOT][2 halves][BM] (int64 bits for INT)
+  double* slot_pred = slot_obs + 2 * NSLOT * BM;                // [NSLOT][BM]
   uint32_t* bias_sm = reinterpret_cast<uint32_t*>(slot_pred + NSLOT * BM);  // [2][BN] bias of a tile
+  uint8_t* w_sm = reinterpret_cast<uint8_t*>(bias_sm + 2 * BN);              // [W_SMEM] checksum w-vector
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -253,10 +256,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 8);
+      mbar_init(&tempty_bar[b], 2 * EPI_WARPS);
     }
     for (int b = 0; b < NSLOT; ++b) {
-      mbar_init(&ofull_bar[b], 4);
+      mbar_init(&ofull_bar[b], EPI_WARPS);
       mbar_init(&oempty_bar[b], 1);
       mbar_init(&pfull_bar[b], 4);
       mbar_init(&pempty_bar[b], 1);
@@ -286,18 +289,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const uint32_t full0 = mapa_shared(smem_u32(&full_bar[0]), 0);  // leader's barriers
       int stage = 0;
       uint32_t phase = 0, chk_pending = 0, chk_phase = 0;
+#ifdef GG_TRACE
+      int plocal = 0;
+#endif
       for (int t = t_first; t < t_end; t += t_step) {
         const int m = t / n_tiles, n = t - m * n_tiles;
         if (!pair_active(m)) continue;
         const int arow = m * 2 * BM + static_cast<int>(rank) * BM;
         const int brow = n * BN + static_cast<int>(rank) * (BN / 2);
         int rem = 0;  // kb % n_tiles
+#ifdef GG_TRACE
+        long long tr_empty = 0, tr_chk = 0;
+#endif
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           const bool mine = PROTECT && rem == n;
           if (++rem == n_tiles) rem = 0;
+#ifdef GG_TRACE
+          const long long tw0 = clock64();
+#endif
           mbar_wait(&empty_bar[stage], phase ^ 1);
+#ifdef GG_TRACE
+          const long long tw1 = clock64();
+          tr_empty += tw1 - tw0;
+#endif
           if (chk_pending & (1u << stage)) {  // the checksum warps still hold the stage's previous K-block
-            mbar_wait(&chkdone_bar[stage], (chk_phase >> stage) & 1u);
+            mbar_wait_spin(&chkdone_bar[stage], (chk_phase >> stage) & 1u);
+#ifdef GG_TRACE
+            tr_chk += clock64() - tw1;
+#endif
             chk_phase ^= 1u << stage;
             chk_pending &= ~(1u << stage);
           }
@@ -308,6 +327,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (mine) chk_pending |= 1u << stage;
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+#ifdef GG_TRACE
+        if (g_trace != nullptr && plocal < TRACE_TILES) {
+          const size_t b = (static_cast<size_t>(blockIdx.x) * TRACE_TILES + plocal) * TRACE_EV;
+          g_trace[b + 17] = tr_empty;
+          g_trace[b + 18] = tr_chk;
+        }
+        ++plocal;
+#endif
       }
     }
   } else if (warp == 1) {
@@ -326,11 +353,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         GG_EV(4, local);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * BN);
+#ifdef GG_TRACE
+        long long tr_full = 0;
+#endif
         int rem = 0;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           const bool mine = PROTECT && rem == n;
           if (++rem == n_tiles) rem = 0;
+#ifdef GG_TRACE
+          const long long tf0 = clock64();
+#endif
           mbar_wait(&full_bar[stage], phase);
+#ifdef GG_TRACE
+          tr_full += clock64() - tf0;
+#endif
           if (mine) {  // both CTAs' halves of this stage have landed: let the checksum warps copy A
             mbar_arrive(&aready_bar[stage]);
             mbar_arrive_cluster(aready_peer + static_cast<uint32_t>(stage * 8));
@@ -348,6 +384,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         tc_commit_pair(&tfull_bar[buf], 0x3);
         GG_EV(5, local);
+#ifdef GG_TRACE
+        if (g_trace != nullptr && local < TRACE_TILES)
+          g_trace[(static_cast<size_t>(blockIdx.x) * TRACE_TILES + local) * TRACE_EV + 19] = tr_full;
+#endif
         ++local;
       }
     }
@@ -379,11 +419,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {  // ascending-tile fold, identical to the split-band fold
               const int i = slot * BM + lane + 32 * q;
+              const int io = 2 * slot * BM + lane + 32 * q;  // half 0, then half 1 (+BM)
               if constexpr (INT) {
-                oi[q] += reinterpret_cast<const long long*>(slot_obs)[i];
+                const long long* so = reinterpret_cast<const long long*>(slot_obs);
+                oi[q] += so[io] + so[io + BM];
                 pi[q] += reinterpret_cast<const long long*>(slot_pred)[i];
               } else {
-                of[q] += slot_obs[i];
+                of[q] += slot_obs[io] + slot_obs[io + BM];
                 pf[q] += slot_pred[i];
               }
             }
@@ -392,7 +434,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int q = 0; q < 4; ++q) {
               const int i = lane + 32 * q;
               const size_t g = static_cast<size_t>(n) * p.m_pad + mb * BM + i;
-              p.ws.partial[g] = slot_obs[slot * BM + i];
+              const int io = 2 * slot * BM + i;
+              if constexpr (INT) {
+                const long long* so = reinterpret_cast<const long long*>(slot_obs);
+                reinterpret_cast<long long*>(p.ws.partial)[g] = so[io] + so[io + BM];
+              } else {
+                p.ws.partial[g] = slot_obs[io] + slot_obs[io + BM];
+              }
               p.ws.pred[g] = slot_pred[slot * BM + i];
             }
           }
@@ -441,11 +489,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         ++local;
       }
     }
-  } else if (warp >= 8) {
-    // ================================================= epilogue (highest warp ids: the SMSP
-    // arbiter issues highest-id-first, so the critical-path warps win every tie)
-    const int eg = warp - 8;            // TMEM lane group (warp % 4) / 32-row slab of this CTA
-    const int tid = threadIdx.x - 256;  // accumulator row within this CTA's 128
+  } else if (warp >= 4 && warp < 12) {
+    // ================================================= epilogue
+    const int e = warp - 4;              // epilogue warp 0..7
+    const int eg = e & 3;                // TMEM lane quadrant (== warp % 4) / 32-row slab of this CTA
+    const int half = e >> 2;             // column half of the tile: chunks 4*half .. 4*half+3
+    const int etid = threadIdx.x - 128;  // 0..255 over the epilogue warps
+    const int tid = eg * 32 + lane;      // accumulator row within this CTA's 128
+    const bool lead = (e == 0 && lane == 0);
     const bool c_tma = p.c_tma != 0 && !p.replay;
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int cbuf = 0;
@@ -457,21 +508,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const uint32_t use = static_cast<uint32_t>(local >> 1);
       // this tile's 256 bias values into shared memory (broadcast reads below; no reliance on L1)
       {
-        uint32_t* bsm = bias_sm + buf * BN;
-        const int c = n * BN + 2 * tid;
+        const int c = n * BN + etid;
         const uint32_t* bg = static_cast<const uint32_t*>(p.bias);
-        bsm[2 * tid] = (bg != nullptr && c < p.N) ? __ldg(bg + c) : 0u;
-        bsm[2 * tid + 1] = (bg != nullptr && c + 1 < p.N) ? __ldg(bg + c + 1) : 0u;
-        named_bar_sync(1, 128);
+        bias_sm[buf * BN + etid] = (bg != nullptr && c < p.N) ? __ldg(bg + c) : 0u;
+        named_bar_sync(1, 32 * EPI_WARPS);
       }
       mbar_wait(&tfull_bar[buf], use & 1);
-      if (tid == 0) GG_EV(0, local);
+      if (lead) GG_EV(0, local);
       tc_fence_after();
       const int row0 = m * 2 * BM + static_cast<int>(rank) * BM;
       const int row = row0 + tid;
       const bool row_ok = row < p.M;
       const int n0 = n * BN;
       const int nchunks = min(BN / 32, (p.N - n0 + 31) / 32);
+      const int c_begin = 4 * half, c_end = min(4 * half + 4, nchunks);
       double obs = 0.0;
       float obs4[4] = {0.f, 0.f, 0.f, 0.f};  // 16-bit outputs: per-tile fp32 chains
       long long obs_i = 0;
@@ -490,18 +540,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } while (0)
 #endif
 #pragma unroll 1
-      for (int c = 0; c < nchunks; ++c) {
+      for (int c = c_begin; c < c_end; ++c) {
         const int col0 = n0 + 32 * c;
         uint32_t r[32];
         tmem_ld_32x32b_x32(
             tmem_base + (static_cast<uint32_t>(eg * 32) << 16) + static_cast<uint32_t>(buf * BN + 32 * c), r);
         tmem_ld_wait();
         GG_LAP(tr_ld);
-        if (c == nchunks - 1) {  // TMEM buffer drained: hand it back to the leader's MMA warp
+        if (c == c_end - 1) {  // this warp's TMEM columns drained: tell the leader's MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tempty0 + static_cast<uint32_t>(buf * 8));
-          if (tid == 0) GG_EV(1, local);
+          if (lead) GG_EV(1, local);
         }
         const bool full = (col0 + 32 <= p.N);
         bool out_inj = false;  // an output fault lands in this row's chunk (rare)
@@ -607,8 +657,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         GG_LAP(tr_obs);
         if (c_tma) {
           // coalesced store: this warp's 32 rows x 32 columns through a swizzled smem box + TMA
-          uint8_t* boxp = smC + (eg * 2 + cbuf) * CST_BYTES;
-          if (lane == 0) bulk_wait_read<1>();  // the box written two chunks ago has been read
+          uint8_t* boxp = smC + e * CST_BYTES + (OUT16 ? cbuf * 2048 : 0);
+          if (lane == 0) {
+            if constexpr (OUT16) bulk_wait_read<1>();  // the box written two chunks ago has been read
+            else bulk_wait_read<0>();
+          }
           __syncwarp();
           stage_row<OUT>(smem_u32(boxp), lane, o);
           fence_proxy_async_smem();
@@ -617,7 +670,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             tma_store_2d(&tmC, boxp, col0, row0 + 32 * eg);
             bulk_commit();
           }
-          cbuf ^= 1;
+          if constexpr (OUT16) cbuf ^= 1;
           GG_LAP(tr_st);
         } else if (row_ok) {
           const long long base = static_cast<long long>(row) * p.ldc + col0;
@@ -630,7 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
         }
       }
-      if (nchunks <= 0) {
+      if (c_begin >= c_end) {  // no columns for this warp in this tile
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty0 + static_cast<uint32_t>(buf * 8));
@@ -642,9 +695,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
       if constexpr (OUT16) obs += (static_cast<double>(obs4[0]) + static_cast<double>(obs4[1])) +
                                  (static_cast<double>(obs4[2]) + static_cast<double>(obs4[3]));
-      if (tid == 0) GG_EV(2, local);
+      if (lead) GG_EV(2, local);
 #ifdef GG_TRACE
-      if (tid == 0 && g_trace != nullptr && local < TRACE_TILES) {
+      if (lead && g_trace != nullptr && local < TRACE_TILES) {
         const size_t b = (static_cast<size_t>(blockIdx.x) * TRACE_TILES + local) * TRACE_EV;
         g_trace[b + 13] = tr_ld;
         g_trace[b + 14] = tr_cmp;
@@ -655,19 +708,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if constexpr (PROTECT) {
         const int slot = local % NSLOT;
         mbar_wait(&oempty_bar[slot], (static_cast<uint32_t>(local / NSLOT) & 1u) ^ 1u);
-        if (tid == 0) GG_EV(3, local);
-        if constexpr (INT) reinterpret_cast<long long*>(slot_obs)[slot * BM + tid] = obs_i;
-        else slot_obs[slot * BM + tid] = obs;
+        if (lead) GG_EV(3, local);
+        const int io = (2 * slot + half) * BM + tid;
+        if constexpr (INT) reinterpret_cast<long long*>(slot_obs)[io] = obs_i;
+        else slot_obs[io] = obs;
         __syncwarp();
         if (lane == 0) mbar_arrive(&ofull_bar[slot]);
       }
       ++local;
     }
     if (c_tma && lane == 0) bulk_wait_all();
-  } else if (warp >= 4 && warp < 8) {
-    // ================================================= checksum producer side
+  } else if (warp >= 12) {
+    // ================================================= checksum producer side (highest warp ids:
+    // the SMSP arbiter issues highest-id-first; these warps are bursty)
     if constexpr (PROTECT) {
-      const int tid = threadIdx.x - 128;  // row within this CTA's 128
+      const int cw = warp - 12;            // rows 32*cw .. 32*cw+31 of this CTA
+      const int ctid = threadIdx.x - 384;  // 0..127
+      const int grp = lane >> 3;           // row within a group of four rows
+      const int sub = lane & 7;            // 16-byte piece of a row's 128-byte K-block
+      // the whole (zero-padded) w-vector into shared memory once, when it fits
+      const void* w_src = p.w_aux;
+      if (p.w_aux_bytes <= W_SMEM) {
+        const uint4* g = static_cast<const uint4*>(p.w_aux);
+        uint4* d = reinterpret_cast<uint4*>(w_sm);
+        for (int i = ctid; i < p.w_aux_bytes / 16; i += 128) d[i] = __ldg(g + i);
+        named_bar_sync(2, 128);
+        w_src = w_sm;
+      }
+      const int tid = ctid;               // row within this CTA's 128
       const int sw = tid & 7;             // 128B-swizzle phase of this row
       int stage = 0;
       uint32_t ar_phase = 0;
@@ -684,27 +752,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const bool mine = (rem == n);
           if (++rem == n_tiles) rem = 0;
           if (!mine) continue;  // this tile's share of the band: K-blocks kb == n (mod n_tiles)
-          mbar_wait(&aready_bar[s], (ar_phase >> s) & 1u);
+          mbar_wait_spin(&aready_bar[s], (ar_phase >> s) & 1u);
           ar_phase ^= 1u << s;
           uint4 v[8];  // this row's 128 B of the stage (16-byte chunk j holds K-bytes 16j..16j+15)
           const uint32_t rowaddr = smem_u32(smA + s * A_BYTES) + static_cast<uint32_t>(tid * 128);
 #pragma unroll
           for (int j = 0; j < 8; ++j) v[j] = lds128(rowaddr + static_cast<uint32_t>((j ^ sw) << 4));
-          fence_proxy_async_smem();  // generic reads of the stage before its TMA refill
+          // these generic-proxy reads must be ordered before the async-proxy (TMA) refill that the
+          // arrive below enables: without the proxy fence the refill can overtake the reads
+          fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&chkdone_bar[s]);
           // w-vectors are zero-padded to whole K-blocks (gg_checksum_aux) and TMA zero-fills
           // x beyond K: no tail checks.  Independent accumulators for ILP.
           if constexpr (INT) {
             // sum_k x*w = sum_d 256^d sum_k x*digit_d(w): exact IDP4A over 128 K per block
-            const int4* dig = static_cast<const int4*>(p.w_aux) + kb * (BK / 4);
+            const int4* dig = static_cast<const int4*>(w_src) + kb * (BK / 4);
             int a[2][3] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const int4 dd = __ldg(dig + j * 4 + q);
+                const int4 dd = dig[j * 4 + q];
                 a[q & 1][0] = __dp4a(static_cast<int>(w4[q]), dd.x, a[q & 1][0]);
                 a[q & 1][1] = __dp4a(static_cast<int>(w4[q]), dd.y, a[q & 1][1]);
                 a[q & 1][2] = __dp4a(static_cast<int>(w4[q]), dd.z, a[q & 1][2]);
@@ -713,11 +783,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             acci += static_cast<long long>(a[0][0] + a[1][0]) + 256ll * (a[0][1] + a[1][1]) +
                     65536ll * (a[0][2] + a[1][2]);
           } else if constexpr (KIND == K_TF32) {
-            const double2* wd = reinterpret_cast<const double2*>(static_cast<const double*>(p.w_aux) + kb * BK);
+            const double2* wd = reinterpret_cast<const double2*>(static_cast<const double*>(w_src) + kb * BK);
             double a[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const double2 w01 = __ldg(wd + 2 * j), w23 = __ldg(wd + 2 * j + 1);
+              const double2 w01 = wd[2 * j], w23 = wd[2 * j + 1];
               a[0] = fma(static_cast<double>(__uint_as_float(v[j].x)), w01.x, a[0]);
               a[1] = fma(static_cast<double>(__uint_as_float(v[j].y)), w01.y, a[1]);
               a[2] = fma(static_cast<double>(__uint_as_float(v[j].z)), w23.x, a[2]);
@@ -725,12 +795,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
             accd += (a[0] + a[1]) + (a[2] + a[3]);
           } else {
-            // bf16/fp16 x is exact in fp32; w = fp32(w_sum) (|w - w_sum| <= 2^-24 |w_sum|).
-            const float4* wq = reinterpret_cast<const float4*>(static_cast<const float*>(p.w_aux) + kb * BK);
+            // bf16/fp16 x is exact in fp32; w = fp32(w_sum) (|w - w_sum| <= 2^-24 |w_sum|)
+            const float4* wq = reinterpret_cast<const float4*>(static_cast<const float*>(w_src) + kb * BK);
             float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const float4 wa = __ldg(wq + 2 * j), wb = __ldg(wq + 2 * j + 1);
+              const float4 wa = wq[2 * j], wb = wq[2 * j + 1];
               float x[8];
               const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
@@ -757,10 +827,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     (static_cast<double>(a[2]) + static_cast<double>(a[3]));
           }
         }
-        if (tid == 0) GG_EV(6, local);
+        if (ctid == 0) GG_EV(6, local);
         const int slot = local % NSLOT;
         mbar_wait(&pempty_bar[slot], (static_cast<uint32_t>(local / NSLOT) & 1u) ^ 1u);
-        if (tid == 0) GG_EV(7, local);
+        if (ctid == 0) GG_EV(7, local);
         if constexpr (INT) reinterpret_cast<long long*>(slot_pred)[slot * BM + tid] = acci;
         else slot_pred[slot * BM + tid] = accd;
         __syncwarp();

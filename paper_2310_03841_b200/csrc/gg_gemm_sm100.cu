@@ -236,6 +236,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.bias = d->bias;
   p.w_sum = d->w_sum;
   p.w_aux = d->w_aux;
+  p.w_aux_bytes = static_cast<int>(checksum_aux_bytes(d->ab_kind, d->K));
   p.bias_sum_f = d->bias_sum_f;
   p.bias_sum_i = d->bias_sum_i;
   p.mu = d->mu;

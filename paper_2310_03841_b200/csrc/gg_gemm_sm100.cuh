@@ -42,7 +42,8 @@ struct Params {
   const void* bias;
   // checksum
   const void* w_sum;    // f64 or i64
-  const void* w_aux;    // bf16/f16: float2 (hi, lo) split of w_sum; i8: int32x4 signed digit planes
+  const void* w_aux;    // gg_checksum_aux encoding (bf16/f16: f32, tf32: f64, i8: int32x4 digit planes)
+  int w_aux_bytes;      // its padded size
   double bias_sum_f;
   long long bias_sum_i;
   double mu, lo, hi;

@@ -15,8 +15,8 @@ b = torch.zeros(N, device='cuda')
 ws, bs = K.offline_checksum(w, b, L.GG_P_F64); aux = K.checksum_aux(ws, torch.bfloat16); bsv = bs.item()
 y = torch.empty(M, N, dtype=torch.bfloat16, device='cuda'); res = K.CheckResult.empty(M, False, 'cuda')
 lib = L.load(); lib.gg_trace_buffer.argtypes = [ctypes.c_void_p]
-TT, EV = 64, 20
-buf = torch.zeros(148 * TT * EV, dtype=torch.int64, device='cuda')
+TT, EV = 64, 24
+buf = torch.zeros(148 * TT * EV + 4 * 64 * 4, dtype=torch.int64, device='cuda')
 run = (lambda: K.protected_gemm(x, w, b, w_sum=ws, w_aux=aux, bias_sum=bsv, lo=-1e30, hi=1e30, out=y, result=res)) \
     if protect else (lambda: K.protected_gemm(x, w, b, protect=False, out=y))
 for _ in range(3): run()
@@ -24,7 +24,17 @@ torch.cuda.synchronize()
 lib.gg_trace_buffer(ctypes.c_void_p(buf.data_ptr()))
 run(); torch.cuda.synchronize()
 lib.gg_trace_buffer(ctypes.c_void_p(0))
-t = buf.view(148, TT, EV).cpu().numpy().astype(np.int64)
+allb = buf.cpu().numpy().astype(np.int64)
+t = allb[:148 * TT * EV].reshape(148, TT, EV)
+det = allb[148 * TT * EV:].reshape(4, 64, 4)
+if os.environ.get('DETAIL'):
+    c = 0
+    base = det[c][det[c] > 0].min() if (det[c] > 0).any() else 0
+    for kb in range(64):
+        r = det[c, kb]
+        if r[3] or r[0]:
+            f = lambda v: v - base if v else -1
+            print(f' kb {kb:2d}: mma full-ok/relay {f(r[3]):7d} | chk wait start {f(r[0]):7d} end {f(r[1]):7d} copy end {f(r[2]):7d}')
 names = {0: 'epi_tfull', 1: 'epi_tmem_rel', 2: 'epi_done', 3: 'epi_slot', 4: 'mma_start', 5: 'mma_end',
          6: 'chk_done', 7: 'chk_slot', 8: 'red_got', 9: 'red_done', 10: 'mma_wait_tempty', 11: 'red_wait', 12: 'red_obs'}
 def stats(cta):
@@ -52,5 +62,14 @@ cp = [t[c, i, 14] for c in range(148) for i in range(TT) if t[c, i, 0] > 0]
 st = [t[c, i, 15] for c in range(148) for i in range(TT) if t[c, i, 0] > 0]
 ob = [t[c, i, 16] for c in range(148) for i in range(TT) if t[c, i, 0] > 0]
 print('epilogue per tile (median cycles): tmem load+wait', np.median(ld), 'convert', np.median(cp), 'obs', np.median(ob), 'stage+tma', np.median(st))
+pe = [t[c, i, 17] for c in range(148) for i in range(TT) if t[c, i, 17] > 0]
+pc = [t[c, i, 18] for c in range(0, 148) for i in range(TT) if t[c, i, 17] > 0]
+mf = [t[c, i, 19] for c in range(0, 148, 2) for i in range(TT) if t[c, i, 4] > 0]
+print('per tile (median cycles): producer wait empty', np.median(pe) if pe else None, 'producer wait chkdone',
+      np.median(pc) if pc else None, 'mma wait full', np.median(mf) if mf else None)
+cw = [t[c, i, 20] for c in range(148) for i in range(TT) if t[c, i, 6] > 0]
+cc = [t[c, i, 21] for c in range(148) for i in range(TT) if t[c, i, 6] > 0]
+cm = [t[c, i, 22] for c in range(148) for i in range(TT) if t[c, i, 6] > 0]
+if cw: print('checksum warps per tile (median cycles): wait aready', np.median(cw), 'copy', np.median(cc), 'compute+other', np.median(cm))
 print('median cycles: mma issue', np.median(mma) if mma else None, 'epilogue', np.median(epi) if epi else None,
       'mma wait tempty', np.median(gapt) if gapt else None)
