@@ -48,6 +48,21 @@ TOKENS = 197
 D, MLP, BLOCKS, CLASSES = 768, 3072, 12, 1000
 CONFIDENCE = 1.0 - 1e-9  # per-row checks: ~50k rows x 50 layers per step => keep false flags << 1 per step
 
+# DRAM bytes (read + write) per protected launch, from `ncu --set full` captures of
+# this kernel (profiles/r01/ncu_full_bf16_vitb.json; profiles/ does not travel to the box)
+NCU_DRAM_MB = {"qkv": 305.4, "proj": 141.1, "fc1": 384.6, "fc2": 382.2}
+
+
+def step_traffic_bytes() -> float:
+    """DRAM traffic of one step (50 launches) measured by ncu; patch embed ~ proj, head ~ 0."""
+    per_block = sum(NCU_DRAM_MB[k] for k in ("qkv", "proj", "fc1", "fc2"))
+    return 1e6 * (NCU_DRAM_MB["proj"] + BLOCKS * per_block)
+
+
+def step_algorithmic_bytes(gemms) -> float:
+    """Minimum bytes of one step: A, B, C of every GEMM in bf16 plus d (8 B) and flags (1 B) per row."""
+    return float(sum(2 * (M * K + N * K + M * N) + 9 * M for _, M, N, K in gemms))
+
 
 def vit_b16_gemms(batch: int = BATCH):
     """(name, M, N, K) of the protected GEMMs of one ViT-B/16 forward."""
@@ -283,7 +298,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "vit_b16_protected_gemm_img_per_s": BATCH * world / (ms_prot * 1e-3),
         "held_out_false_flags": false_flags,
         "roofline": {"bound": "tensor", "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s",
-                     "frac": per_gpu / peak, "traffic": None,
+                     "frac": per_gpu / peak, "traffic": step_traffic_bytes(),
+                     "traffic_unit": "DRAM bytes per step (50 launches), ncu --set full",
+                     "algorithmic_bytes": step_algorithmic_bytes(gemms),
+                     "hbm_gbs_achieved": step_traffic_bytes() / (ms_prot * 1e-3) / 1e9,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, back to back 4 s)",
                      "kernel": "gg_protected_gemm_kernel<bf16,bf16,protect> (the only kernel in the step)"},
         "e2e": e2e,
