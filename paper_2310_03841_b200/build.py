@@ -87,19 +87,20 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
-def build_trace(verbose: bool = False) -> Path:
-    """Diagnostics build (-DGG_TRACE): per-tile clock64 stamps of every warp role;
-    never loaded by the product (select it with $GEMMGUARD_LIB)."""
+def build_variant(name: str, defines: list[str]) -> Path:
+    """Diagnostics / A-B build with extra preprocessor defines, linked to
+    _build/libgemmguard_b200_<name>.so; never loaded by the product (select it
+    with $GEMMGUARD_LIB)."""
     BUILD.mkdir(exist_ok=True)
     objs = []
     for src in SOURCES:
-        obj = BUILD / (Path(src).stem + ".trace.o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-DGG_TRACE", "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
+        obj = BUILD / f"{Path(src).stem}.{name}.o"
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *defines, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr[-6000:]}")
         objs.append(obj)
-    out = BUILD / "libgemmguard_b200_trace.so"
+    out = BUILD / f"libgemmguard_b200_{name}.so"
     res = subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(out), *map(str, objs), "-lcuda"],
                          capture_output=True, text=True)
     if res.returncode != 0:
@@ -107,11 +108,20 @@ def build_trace(verbose: bool = False) -> Path:
     return out
 
 
+def build_trace(verbose: bool = False) -> Path:
+    """-DGG_TRACE: per-tile clock64 stamps of every warp role (tools/trace_tiles.py)."""
+    return build_variant("trace", ["-DGG_TRACE"])
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--trace", action="store_true", help="also build the diagnostics library")
+    ap.add_argument("--variant", nargs="+", metavar=("NAME", "DEFINE"),
+                    help="also build _build/libgemmguard_b200_NAME.so with -DDEFINE for each DEFINE")
     a = ap.parse_args()
     print(build(force=a.force, verbose=True))
     if a.trace:
         print(build_trace(verbose=True))
+    if a.variant:
+        print(build_variant(a.variant[0], [f"-D{d}" for d in a.variant[1:]]))

@@ -20,6 +20,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// Release-add at GPU scope: this thread's prior writes (and those it has observed, e.g.
+// through __syncwarp) are visible before the increment.  No sequentially consistent
+// fence and no L1 invalidation (a __threadfence() is MEMBAR.SC.GPU + CCTL.IVALL).
+__device__ __forceinline__ int atom_add_release_gpu(int* addr, int v) {
+  int old;
+  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
+  return old;
+}
+// Acquire side of the counter protocol (taken only by the last arriver).
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -265,6 +275,19 @@ __device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) {
       : "=l"(r)
       : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
   return *reinterpret_cast<float2*>(&r);
+}
+// packed fp32 pair FMA (sm_100: FFMA2)
+__device__ __forceinline__ float2 fma_f32x2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+// packed bf16 pair -> two fp32 (lo from bits 0-15) on the ALU pipe (PRMT + LOP3, no IMAD)
+__device__ __forceinline__ float2 bf16x2_to_f32x2(uint32_t w) {
+  return make_float2(__uint_as_float(__byte_perm(w, 0u, 0x1054u)), __uint_as_float(w & 0xFFFF0000u));
 }
 // two fp32 -> packed 16-bit pair, round to nearest even (lo in bits 0-15)
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

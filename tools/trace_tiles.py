@@ -70,6 +70,7 @@ print('per tile (median cycles): producer wait empty', np.median(pe) if pe else 
 cw = [t[c, i, 20] for c in range(148) for i in range(TT) if t[c, i, 6] > 0]
 cc = [t[c, i, 21] for c in range(148) for i in range(TT) if t[c, i, 6] > 0]
 cm = [t[c, i, 22] for c in range(148) for i in range(TT) if t[c, i, 6] > 0]
-if cw: print('checksum warps per tile (median cycles): wait aready', np.median(cw), 'copy', np.median(cc), 'compute+other', np.median(cm))
+cu = [t[c, i, 23] for c in range(148) for i in range(TT) if t[c, i, 6] > 0]
+if cw: print('checksum warps per tile (median cycles): wait aready', np.median(cw), 'copy(lds)', np.median(cc), 'fence+arrive', np.median(cm), 'compute', np.median(cu))
 print('median cycles: mma issue', np.median(mma) if mma else None, 'epilogue', np.median(epi) if epi else None,
       'mma wait tempty', np.median(gapt) if gapt else None)
