@@ -98,32 +98,34 @@ __device__ __forceinline__ void pair_range(int pid, int npairs, int total, int& 
 template <bool INT>
 __device__ void finish_band(const Params& p, int mb, int lane, const double (&obs_f)[4], const double (&pred_f)[4],
                             const long long (&obs_i)[4], const long long (&pred_i)[4]) {
+  const bool per_sample = INT || p.statistic == GG_PER_SAMPLE;
+  const bool bmean = !INT && p.statistic == GG_BATCH_MEAN;
   int nflag = 0;
   unsigned long long key = 0;
+  unsigned long long dbits[4];  // d of rows lane + 32q (f64 or i64 bits)
+  bool flag[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int row = mb * BM + lane + 32 * q;
+    flag[q] = false;
+    dbits[q] = 0;
     if (row >= p.M) continue;
-    bool flag;
     if constexpr (INT) {
       const long long di = (pred_i[q] + p.bias_sum_i) - obs_i[q];
-      static_cast<long long*>(p.d)[row] = di;
-      flag = di != 0;
+      dbits[q] = static_cast<unsigned long long>(di);
+      flag[q] = di != 0;
       const unsigned long long mag =
           di < 0 ? 0ull - static_cast<unsigned long long>(di) : static_cast<unsigned long long>(di);
       const unsigned long long k = gap_key(static_cast<double>(mag));
       key = k > key ? k : key;
     } else {
       const double dd = (pred_f[q] + p.bias_sum_f) - obs_f[q];
-      static_cast<double*>(p.d)[row] = dd;
-      flag = !((dd >= p.lo) && (dd <= p.hi));
+      dbits[q] = static_cast<unsigned long long>(__double_as_longlong(dd));
+      flag[q] = !((dd >= p.lo) && (dd <= p.hi));
       const unsigned long long k = gap_key(fabs(dd - p.mu));
       key = k > key ? k : key;
     }
-    if (INT || p.statistic == GG_PER_SAMPLE) {
-      p.flags[row] = flag ? 1 : 0;
-      nflag += flag ? 1 : 0;
-    }
+    if (per_sample) nflag += flag[q] ? 1 : 0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -131,33 +133,47 @@ __device__ void finish_band(const Params& p, int mb, int lane, const double (&ob
     const unsigned long long w = __shfl_xor_sync(0xffffffffu, key, o);
     key = w > key ? w : key;
   }
-  int last = 0;
-  if (lane == 0) {
-    p.ws.band_nflag[mb] = nflag;
-    p.ws.band_maxkey[mb] = key;
+  auto store_rows = [&]() {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int row = mb * BM + lane + 32 * q;
+      if (row >= p.M) continue;
+      static_cast<unsigned long long*>(p.d)[row] = dbits[q];
+      if (per_sample) p.flags[row] = flag[q] ? 1 : 0;
+    }
+    if (lane == 0) {
+      p.ws.band_nflag[mb] = nflag;
+      p.ws.band_maxkey[mb] = key;
+    }
+  };
+  // Launch summary: atomicMax of the band's gap key, then a release-add of
+  // {1 << 32 | flagged rows}; the band that completes the count acquires and reads the
+  // totals.  The release has no outstanding stores to wait for when the rows are stored
+  // after it (the batch-mean statistic reads every row's d, so there they go first).
+  if (bmean) {
+    store_rows();
+    __syncwarp();
   }
-  __syncwarp();  // the warp's d / flags / summary writes, then lane 0 releases them with the count
+  int last = 0;
+  unsigned long long fin_rows = 0, fin_key = 0;
   if (lane == 0) {
     const int total = p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles;
-    last = (atom_add_release_gpu(&p.ws.counters[0], 1) == total - 1) ? 1 : 0;
-    if (last) fence_acquire_gpu();
+    atomicMax(&p.ws.summary[1], key);
+    const unsigned long long inc = (1ull << 32) | static_cast<unsigned>(nflag);
+    const unsigned long long old = atom_add_release_gpu_u64(&p.ws.summary[0], inc);
+    last = (static_cast<long long>(old >> 32) + 1 == total) ? 1 : 0;
+    if (last) {
+      fence_acquire_gpu();
+      fin_rows = (old + inc) & 0xFFFFFFFFull;
+      fin_key = atomicMax(&p.ws.summary[1], 0ull);
+    }
   }
+  if (!bmean) store_rows();
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
-  int nf = 0;
-  unsigned long long mk = 0;
-  for (int b = lane; b < p.m_tiles; b += 32) {
-    nf += __ldcg(&p.ws.band_nflag[b]);
-    const unsigned long long k = __ldcg(&p.ws.band_maxkey[b]);
-    mk = k > mk ? k : mk;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nf += __shfl_xor_sync(0xffffffffu, nf, o);
-    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mk, o);
-    mk = w > mk ? w : mk;
-  }
-  if (!INT && p.statistic == GG_BATCH_MEAN) {
+  int nf = static_cast<int>(__shfl_sync(0xffffffffu, fin_rows, 0));
+  const unsigned long long mk = __shfl_sync(0xffffffffu, fin_key, 0);
+  if (bmean) {
     double s = 0.0;  // fixed lane -> row assignment and shuffle tree: deterministic
     for (int r = lane; r < p.M; r += 32) s += ldcg_f64(&static_cast<double*>(p.d)[r]);
 #pragma unroll
@@ -172,9 +188,49 @@ __device__ void finish_band(const Params& p, int mb, int lane, const double (&ob
     *p.triggered = nf > 0 ? 1 : 0;
     *p.max_disc = (mk == 0ull) ? __longlong_as_double(0x7FF0000000000000ll)
                                : __longlong_as_double(static_cast<long long>(mk - 1ull));
-    p.ws.counters[0] = 0;
-    __threadfence();
+    p.ws.summary[0] = 0ull;  // every band has counted: the workspace is left ready
+    p.ws.summary[1] = 0ull;
   }
+}
+
+// Error-free fp32 accumulation: (hi, lo) += x with hi + lo exact up to lo's own rounding.
+__device__ __forceinline__ void two_sum_acc(float& hi, float& lo, float x) {
+  const float t = hi + x, bp = t - hi;
+  lo += (hi - (t - bp)) + (x - bp);
+  hi = t;
+}
+
+// Partial sums travel as 8-byte values in one of three representations (ring slots,
+// workspace partials, reducer accumulators): int64 (int8 operands), an fp32 (hi, lo)
+// double-float pair (16-bit operand / output paths: no FP64 instruction per tile, whose
+// issue is slow next to the tensor pipe), or fp64 (fp32 paths).
+enum { ACC_I64 = 0, ACC_DF = 1, ACC_F64 = 2 };
+template <int MODE>
+__device__ __forceinline__ unsigned long long acc_add(unsigned long long a, unsigned long long b) {
+  if constexpr (MODE == ACC_I64) {
+    return static_cast<unsigned long long>(static_cast<long long>(a) + static_cast<long long>(b));
+  } else if constexpr (MODE == ACC_DF) {  // (ah, al) + (bh, bl), relative error ~2^-44
+    const float ah = __uint_as_float(static_cast<uint32_t>(a)), al = __uint_as_float(static_cast<uint32_t>(a >> 32));
+    const float bh = __uint_as_float(static_cast<uint32_t>(b)), bl = __uint_as_float(static_cast<uint32_t>(b >> 32));
+    const float sh = ah + bh, bp = sh - ah;
+    float e = (ah - (sh - bp)) + (bh - bp);
+    e += al + bl;
+    const float h = sh + e, l = e - (h - sh);
+    return static_cast<unsigned long long>(__float_as_uint(h)) |
+           (static_cast<unsigned long long>(__float_as_uint(l)) << 32);
+  } else {
+    return static_cast<unsigned long long>(
+        __double_as_longlong(__longlong_as_double(static_cast<long long>(a)) +
+                             __longlong_as_double(static_cast<long long>(b))));
+  }
+}
+template <int MODE>
+__device__ __forceinline__ double acc_f64(unsigned long long a) {
+  if constexpr (MODE == ACC_DF)
+    return static_cast<double>(__uint_as_float(static_cast<uint32_t>(a))) +
+           static_cast<double>(__uint_as_float(static_cast<uint32_t>(a >> 32)));
+  else
+    return __longlong_as_double(static_cast<long long>(a));
 }
 
 // 16 bytes of the checksum w-vector encoding at byte offset `off`: an explicit
@@ -243,10 +299,7 @@ __device__ __forceinline__ void chk_dot(const uint4 (&v)[8], int kb, uint32_t w_
         a[q & 1] = fma_f32x2(x, wp[q], a[q & 1]);
       }
     }
-    const float sb = (a[0].x + a[0].y) + (a[1].x + a[1].y);
-    const float t = hi + sb, bp = t - hi;
-    lo += (hi - (t - bp)) + (sb - bp);
-    hi = t;
+    two_sum_acc(hi, lo, (a[0].x + a[0].y) + (a[1].x + a[1].y));
   }
 }
 
@@ -278,6 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   constexpr int MMA_K_BYTES = 32;
   constexpr int MMAS_PER_STAGE = BK_BYTES / MMA_K_BYTES;
   constexpr bool OUT16 = (OUT == O_BF16 || OUT == O_F16);
+  constexpr bool PRED_PAIR = (KIND == K_BF16 || KIND == K_F16);  // predicted partials as fp32 (hi, lo)
   constexpr uint32_t IDESC = PairIdesc<KIND>::V;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -306,14 +360,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t rank = cluster_ctarank();
   const int n_tiles = p.n_tiles;
   const int m_pairs = (p.M + 2 * BM - 1) / (2 * BM);
-  // tiles t = t_first, t_first + t_step, ... < t_end: a contiguous range per pair (bands folded
-  // locally) or, when the concurrently streamed A bands would not fit in L2, a strided walk
+  // The pair's tiles: a contiguous range [t0, t1) (bands folded locally) or, when the
+  // concurrently streamed A bands would not fit in L2, a strided walk.  A contiguous range
+  // is walked as: its leading partial band, its trailing partial band, then its whole bands,
+  // so the partial bands' exchange with the neighbouring pairs completes early, off the
+  // end of the launch.
   const int pid = static_cast<int>(blockIdx.x >> 1), npairs = static_cast<int>(gridDim.x >> 1);
   int t0, t1;
   pair_range(pid, npairs, m_pairs * n_tiles, t0, t1);
-  const int t_first = p.sched ? pid : t0;
-  const int t_end = p.sched ? m_pairs * n_tiles : t1;
-  const int t_step = p.sched ? npairs : 1;
+  const int hb = min((t0 + n_tiles - 1) / n_tiles * n_tiles, t1);  // end of the leading partial band
+  const int tb = max(t1 / n_tiles * n_tiles, hb);                  // start of the trailing partial band
+  const int n_seq = p.sched ? (m_pairs * n_tiles - pid + npairs - 1) / npairs : t1 - t0;
+  auto tile_at = [&](int i) -> int {
+    if (p.sched) return pid + i * npairs;
+    if (i < hb - t0) return t0 + i;
+    i -= hb - t0;
+    if (i < t1 - tb) return tb + i;
+    return hb + (i - (t1 - tb));
+  };
 
   // warp roles; the SMSP arbiter issues highest-warp-id first, so the ids follow criticality
   constexpr int W_MMA = 15, W_PRODUCER = 14, W_ALLOC = 13, W_REDUCER = 12, W_CHK0 = 8, W_EPI0 = 0;
@@ -365,7 +429,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #ifdef GG_TRACE
       int plocal = 0;
 #endif
-      for (int t = t_first; t < t_end; t += t_step) {
+      for (int i_seq = 0; i_seq < n_seq; ++i_seq) {
+        const int t = tile_at(i_seq);
         const int m = t / n_tiles, n = t - m * n_tiles;
         if (!pair_active(m)) continue;
         const int arow = m * 2 * BM + static_cast<int>(rank) * BM;
@@ -417,7 +482,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = t_first; t < t_end; t += t_step) {
+      for (int i_seq = 0; i_seq < n_seq; ++i_seq) {
+        const int t = tile_at(i_seq);
         const int m = t / n_tiles, n = t - m * n_tiles;
         if (!pair_active(m)) continue;
         const int buf = local & 1;
@@ -467,10 +533,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else if (warp == W_REDUCER) {
     // ================================================= reducer
     if constexpr (PROTECT) {
-      double of[4] = {0.0, 0.0, 0.0, 0.0}, pf[4] = {0.0, 0.0, 0.0, 0.0};
-      long long oi[4] = {0, 0, 0, 0}, pi[4] = {0, 0, 0, 0};
+      constexpr int OBS_MODE = INT ? ACC_I64 : (OUT16 ? ACC_DF : ACC_F64);
+      constexpr int PRED_MODE = INT ? ACC_I64 : (PRED_PAIR ? ACC_DF : ACC_F64);
+      const unsigned long long* so = reinterpret_cast<const unsigned long long*>(slot_obs);
+      const unsigned long long* sp = reinterpret_cast<const unsigned long long*>(slot_pred);
+      unsigned long long* gpart = reinterpret_cast<unsigned long long*>(p.ws.partial);
+      unsigned long long* gpred = reinterpret_cast<unsigned long long*>(p.ws.pred);
+      // d / flags of a folded band (one conversion to fp64 per row and band)
+      auto finish = [&](int mb, const unsigned long long (&ao)[4], const unsigned long long (&ap)[4]) {
+        double of[4], pf[4];
+        long long oi[4], pi[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          oi[q] = static_cast<long long>(ao[q]);
+          pi[q] = static_cast<long long>(ap[q]);
+          of[q] = INT ? 0.0 : acc_f64<OBS_MODE>(ao[q]);
+          pf[q] = INT ? 0.0 : acc_f64<PRED_MODE>(ap[q]);
+        }
+        finish_band<INT>(p, mb, lane, of, pf, oi, pi);
+      };
+      unsigned long long ao[4] = {0ull, 0ull, 0ull, 0ull}, ap[4] = {0ull, 0ull, 0ull, 0ull};
       int local = 0;
-      for (int t = t_first; t < t_end; t += t_step) {
+      for (int i_seq = 0; i_seq < n_seq; ++i_seq) {
+        const int t = tile_at(i_seq);
         const int m = t / n_tiles, n = t - m * n_tiles;
         if (!pair_active(m)) continue;
         const int slot = local % NSLOT;
@@ -484,37 +569,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const bool band_ok = mb < p.m_tiles && (!p.replay || p.ws.band_active[mb]) && !(p.dbg & 4);
         const bool whole = !p.sched && (m * n_tiles >= t0) && ((m + 1) * n_tiles <= t1);  // band folded locally
         if (band_ok) {
-          if (whole) {
-            if (n == 0) {
+          if (whole && n == 0) {
 #pragma unroll
-              for (int q = 0; q < 4; ++q) { of[q] = 0.0; pf[q] = 0.0; oi[q] = 0; pi[q] = 0; }
-            }
+            for (int q = 0; q < 4; ++q) { ao[q] = 0ull; ap[q] = 0ull; }
+          }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {  // ascending-tile fold, identical to the split-band fold
-              const int i = slot * BM + lane + 32 * q;
-              const int io = 2 * slot * BM + lane + 32 * q;  // half 0, then half 1 (+BM)
-              if constexpr (INT) {
-                const long long* so = reinterpret_cast<const long long*>(slot_obs);
-                oi[q] += so[io] + so[io + BM];
-                pi[q] += reinterpret_cast<const long long*>(slot_pred)[i];
-              } else {
-                of[q] += slot_obs[io] + slot_obs[io + BM];
-                pf[q] += slot_pred[i];
-              }
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int i = lane + 32 * q;
+          for (int q = 0; q < 4; ++q) {
+            const int i = lane + 32 * q;
+            const int io = 2 * slot * BM + i;  // half 0, then half 1 (+BM)
+            // this tile's observed partial (both column halves) and predicted partial; the
+            // ascending-tile fold below is the same for local and split bands
+            const unsigned long long to = acc_add<OBS_MODE>(so[io], so[io + BM]);
+            const unsigned long long tp = sp[slot * BM + i];
+            if (whole) {
+              ao[q] = acc_add<OBS_MODE>(ao[q], to);
+              ap[q] = acc_add<PRED_MODE>(ap[q], tp);
+            } else {
               const size_t g = static_cast<size_t>(n) * p.m_pad + mb * BM + i;
-              const int io = 2 * slot * BM + i;
-              if constexpr (INT) {
-                const long long* so = reinterpret_cast<const long long*>(slot_obs);
-                reinterpret_cast<long long*>(p.ws.partial)[g] = so[io] + so[io + BM];
-              } else {
-                p.ws.partial[g] = slot_obs[io] + slot_obs[io + BM];
-              }
-              p.ws.pred[g] = slot_pred[slot * BM + i];
+              gpart[g] = to;
+              gpred[g] = tp;
             }
           }
         }
@@ -525,12 +598,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         if (band_ok) {
           if (whole) {
-            if (n == n_tiles - 1) finish_band<INT>(p, mb, lane, of, pf, oi, pi);
-          } else {
-            __syncwarp();  // this tile's partials, released by lane 0 with the band count
+            if (n == n_tiles - 1) finish(mb, ao, ap);
+          } else if (p.sched || t == min((m + 1) * n_tiles, t1) - 1) {
+            // the pair's last tile of this band: release its partials with one count of the
+            // tiles it contributed (contiguous schedule: at most two such parts per pair)
+            const int part = p.sched ? 1 : min((m + 1) * n_tiles, t1) - max(m * n_tiles, t0);
+            __syncwarp();
             int last = 0;
             if (lane == 0) {
-              last = (atom_add_release_gpu(&p.ws.band_counter[mb], 1) == n_tiles - 1) ? 1 : 0;
+              last = (atom_add_release_gpu(&p.ws.band_counter[mb], part) == n_tiles - part) ? 1 : 0;
               if (last) {
                 fence_acquire_gpu();  // the other pairs' partials
                 p.ws.band_counter[mb] = 0;
@@ -538,22 +614,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
             last = __shfl_sync(0xffffffffu, last, 0);
             if (last) {
-              double sof[4] = {0.0, 0.0, 0.0, 0.0}, spf[4] = {0.0, 0.0, 0.0, 0.0};
-              long long soi[4] = {0, 0, 0, 0}, spi[4] = {0, 0, 0, 0};
-              for (int tt = 0; tt < n_tiles; ++tt) {
+              unsigned long long bo[4] = {0ull, 0ull, 0ull, 0ull}, bpr[4] = {0ull, 0ull, 0ull, 0ull};
+              // ascending-tile fold; the loads of four tiles are in flight together
+              for (int tt0 = 0; tt0 < n_tiles; tt0 += 4) {
+                unsigned long long vo[4][4], vp[4][4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const size_t g = static_cast<size_t>(tt) * p.m_pad + mb * BM + lane + 32 * q;
-                  if constexpr (INT) {
-                    soi[q] += ldcg_i64(reinterpret_cast<const long long*>(p.ws.partial) + g);
-                    spi[q] += ldcg_i64(reinterpret_cast<const long long*>(p.ws.pred) + g);
-                  } else {
-                    sof[q] += ldcg_f64(p.ws.partial + g);
-                    spf[q] += ldcg_f64(p.ws.pred + g);
+                for (int j = 0; j < 4; ++j) {
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    vo[j][q] = 0ull;
+                    vp[j][q] = 0ull;
+                    if (tt0 + j < n_tiles) {
+                      const size_t g = static_cast<size_t>(tt0 + j) * p.m_pad + mb * BM + lane + 32 * q;
+                      vo[j][q] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpart + g)));
+                      vp[j][q] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpred + g)));
+                    }
+                  }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  if (tt0 + j >= n_tiles) break;
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    bo[q] = acc_add<OBS_MODE>(bo[q], vo[j][q]);
+                    bpr[q] = acc_add<PRED_MODE>(bpr[q], vp[j][q]);
                   }
                 }
               }
-              finish_band<INT>(p, mb, lane, sof, spf, soi, spi);
+              finish(mb, bo, bpr);
             }
           }
         }
@@ -576,12 +664,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // bias of a tile's 256 columns, one value per epilogue thread, loaded one tile ahead (its
     // latency is off the critical path) and staged in shared memory for the broadcast reads below
     const uint32_t* bias_g = static_cast<const uint32_t*>(p.bias);
-    auto bias_of = [&](int tt) -> uint32_t {
-      const int c = (tt % n_tiles) * BN + etid;
-      return (bias_g != nullptr && tt < t_end && c < p.N) ? __ldcg(bias_g + c) : 0u;
+    auto bias_of = [&](int i) -> uint32_t {  // bias value of this thread's column in the i-th tile
+      if (bias_g == nullptr || i >= n_seq) return 0u;
+      const int c = (tile_at(i) % n_tiles) * BN + etid;
+      return c < p.N ? __ldcg(bias_g + c) : 0u;
     };
-    uint32_t bias_next = bias_of(t_first);
-    for (int t = t_first; t < t_end; t += t_step) {
+    uint32_t bias_next = bias_of(0);
+    for (int i_seq = 0; i_seq < n_seq; ++i_seq) {
+        const int t = tile_at(i_seq);
       const int m = t / n_tiles, n = t - m * n_tiles;
       if (!pair_active(m)) continue;
       const int buf = local & 1;
@@ -591,7 +681,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const uint32_t bcur = bias_next;
         const int c = n * BN + etid;
         bias_sm[buf * BN + etid] = (p.replay && bias_g != nullptr && c < p.N) ? __ldcg(bias_g + c) : bcur;
-        bias_next = bias_of(t + t_step);
+        bias_next = bias_of(i_seq + 1);
         named_bar_sync(1, 32 * EPI_WARPS);
       }
       mbar_wait(&tfull_bar[buf], use & 1);
@@ -768,11 +858,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int o2 = 16; o2 > 0; o2 >>= 1) changed += __shfl_xor_sync(0xffffffffu, changed, o2);
         if (lane == 0 && changed) atomicAdd(p.changed, changed);
       }
-      if constexpr (OUT16)
-        obs += ((static_cast<double>(obs_a.x) + static_cast<double>(obs_a.y)) +
-                (static_cast<double>(obs_b.x) + static_cast<double>(obs_b.y))) +
-               ((static_cast<double>(obs4[0]) + static_cast<double>(obs4[1])) +
-                (static_cast<double>(obs4[2]) + static_cast<double>(obs4[3])));
+      float obs_hi = 0.f, obs_lo = 0.f;  // 16-bit outputs: the chains folded exactly, no FP64 here
+      if constexpr (OUT16) {
+        obs_hi = obs_a.x;
+        two_sum_acc(obs_hi, obs_lo, obs_a.y);
+        two_sum_acc(obs_hi, obs_lo, obs_b.x);
+        two_sum_acc(obs_hi, obs_lo, obs_b.y);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) two_sum_acc(obs_hi, obs_lo, obs4[j]);
+      }
       if (lead) GG_EV(2, local);
 #ifdef GG_TRACE
       if (lead && g_trace != nullptr && local < TRACE_TILES) {
@@ -789,6 +883,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lead) GG_EV(3, local);
         const int io = (2 * slot + half) * BM + tid;
         if constexpr (INT) reinterpret_cast<long long*>(slot_obs)[io] = obs_i;
+        else if constexpr (OUT16) reinterpret_cast<float2*>(slot_obs)[io] = make_float2(obs_hi, obs_lo);
         else slot_obs[io] = obs;
         __syncwarp();
         if (lane == 0) mbar_arrive(&ofull_bar[slot]);
@@ -854,7 +949,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #endif
       };
       int local = 0;
-      for (int t = t_first; t < t_end; t += t_step) {
+      for (int i_seq = 0; i_seq < n_seq; ++i_seq) {
+        const int t = tile_at(i_seq);
         const int m = t / n_tiles, n = t - m * n_tiles;
         if (!pair_active(m)) continue;
         double accd = 0.0;
@@ -883,7 +979,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           tc_comp += clock64() - cp0;
 #endif
         }
-        if constexpr (KIND == K_BF16 || KIND == K_F16) accd = static_cast<double>(hi) + static_cast<double>(lo);
         st0 = (st0 + p.k_blocks) % STAGES;
         if (ctid == 0) GG_EV(6, local);
 #ifdef GG_TRACE
@@ -900,6 +995,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         mbar_wait(&pempty_bar[slot], (static_cast<uint32_t>(local / NSLOT) & 1u) ^ 1u);
         if (ctid == 0) GG_EV(7, local);
         if constexpr (INT) reinterpret_cast<long long*>(slot_pred)[slot * BM + tid] = acci;
+        else if constexpr (KIND == K_BF16 || KIND == K_F16)
+          reinterpret_cast<float2*>(slot_pred)[slot * BM + tid] = make_float2(hi, lo);
         else slot_pred[slot * BM + tid] = accd;
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull_bar[slot]);

@@ -74,7 +74,7 @@ int num_sms() {
 }
 
 struct WsLayout {
-  size_t counters, band_counter, band_active, band_nflag, band_maxkey, pred, partial, total;
+  size_t summary, counters, band_counter, band_active, band_nflag, band_maxkey, pred, partial, total;
 };
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 WsLayout ws_layout(int64_t M, int64_t N) {
@@ -83,6 +83,7 @@ WsLayout ws_layout(int64_t M, int64_t N) {
   const size_t m_pad = m_tiles * BM;
   WsLayout L{};
   size_t off = 0;
+  L.summary = off; off += 16;
   L.counters = off; off = align_up(off + 16, 256);
   L.band_counter = off; off = align_up(off + 4 * m_tiles, 256);
   L.band_active = off; off = align_up(off + m_tiles, 256);
@@ -94,11 +95,20 @@ WsLayout ws_layout(int64_t M, int64_t N) {
   return L;
 }
 
+// Replay: mark the 128-row bands holding flagged rows and seed the launch summary with the
+// inactive bands' standing summaries (the replayed bands add theirs); with no active band
+// the summary is final here.
 __global__ void replay_prepare_kernel(const uint8_t* rows, int M, int m_tiles, uint8_t* band_active, int* counters,
-                                      int* changed) {
-  // one warp per band; one block does the count
-  __shared__ int s_count;
-  if (threadIdx.x == 0) s_count = 0;
+                                      unsigned long long* summary, const int* band_nflag,
+                                      const unsigned long long* band_maxkey, int* changed, int* nflag,
+                                      uint8_t* triggered, double* max_disc) {
+  __shared__ int s_count, s_rows;
+  __shared__ unsigned long long s_key;
+  if (threadIdx.x == 0) {
+    s_count = 0;
+    s_rows = 0;
+    s_key = 0ull;
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int m = warp; m < m_tiles; m += nw) {
@@ -107,14 +117,27 @@ __global__ void replay_prepare_kernel(const uint8_t* rows, int M, int m_tiles, u
     any = __any_sync(0xffffffffu, any);
     if (lane == 0) {
       band_active[m] = any ? 1 : 0;
-      if (any) atomicAdd(&s_count, 1);
+      if (any) {
+        atomicAdd(&s_count, 1);
+      } else {
+        atomicAdd(&s_rows, band_nflag[m]);
+        atomicMax(&s_key, band_maxkey[m]);
+      }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    counters[0] = 0;
     counters[1] = s_count;
     if (changed) *changed = 0;
+    if (s_count > 0) {
+      summary[0] = static_cast<unsigned long long>(static_cast<unsigned>(s_rows));
+      summary[1] = s_key;
+    } else {
+      *nflag = s_rows;
+      *triggered = s_rows > 0 ? 1 : 0;
+      *max_disc = (s_key == 0ull) ? __longlong_as_double(0x7FF0000000000000ll)
+                                  : __longlong_as_double(static_cast<long long>(s_key - 1ull));
+    }
   }
 }
 
@@ -256,6 +279,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   if (protect) {
     const WsLayout L = ws_layout(d->M, d->N);
     uint8_t* w = static_cast<uint8_t*>(d->workspace);
+    p.ws.summary = reinterpret_cast<unsigned long long*>(w + L.summary);
     p.ws.counters = reinterpret_cast<int*>(w + L.counters);
     p.ws.band_counter = reinterpret_cast<int*>(w + L.band_counter);
     p.ws.band_active = w + L.band_active;
@@ -266,7 +290,8 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   }
   if (replay) {
     replay_prepare_kernel<<<1, 1024, 0, s>>>(d->replay_rows, p.M, p.m_tiles, p.ws.band_active, p.ws.counters,
-                                              d->changed);
+                                              p.ws.summary, p.ws.band_nflag, p.ws.band_maxkey, d->changed,
+                                              d->nflag, d->triggered, d->max_disc);
     rc = check_launch("replay_prepare");
     if (rc) return rc;
   }
@@ -276,6 +301,8 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   // A bands streamed concurrently by all pairs (256 rows x K each): keep them L2-resident
   const double a_footprint = static_cast<double>(pairs) * 2 * pair::BM * static_cast<double>(d->K) * elem;
   p.sched = a_footprint > 40.0e6 ? 1 : 0;
+  if (p.dbg & 1024) p.sched = 0;  // diagnostics: force a schedule
+  if (p.dbg & 2048) p.sched = 1;
 
   switch (kind) {
     case K_BF16:

@@ -23,7 +23,8 @@ enum : int { K_BF16 = 0, K_F16 = 1, K_TF32 = 2, K_I8 = 3 };
 enum : int { O_BF16 = 0, O_F16 = 1, O_F32 = 2, O_I32 = 3 };
 
 struct Workspace {
-  int* counters;        // [0] done bands, [1] active bands
+  unsigned long long* summary;  // [2] {done bands << 32 | flagged rows, max gap key}: one 128-bit CAS per band
+  int* counters;        // [1] active bands (replay)
   int* band_counter;    // [m_tiles]
   uint8_t* band_active; // [m_tiles]
   int* band_nflag;      // [m_tiles]
@@ -57,7 +58,9 @@ struct Params {
   int n_inj;
   int c_tma;            // 1: C is stored through smem boxes + TMA (needs 16 B aligned C and pitch)
   int sched;            // 0: contiguous tile range per pair, 1: strided (long K)
-  int dbg;              // diagnostics only ($GG_DEBUG), 0 in production
+  int dbg;              // diagnostics only ($GG_DEBUG), 0 in production: 1 skip predicted dot products,
+                        // 2 decouple the checksum warps from the stages, 4 skip band folds, 8 skip
+                        // observed sums, 1024 / 2048 force the contiguous / strided schedule
   int replay;           // 1: only active bands, compare against old C
   int* changed;
   Workspace ws;

@@ -28,6 +28,12 @@ __device__ __forceinline__ int atom_add_release_gpu(int* addr, int v) {
   asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ unsigned long long atom_add_release_gpu_u64(unsigned long long* addr,
+                                                                      unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.release.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(addr), "l"(v) : "memory");
+  return old;
+}
 // Acquire side of the counter protocol (taken only by the last arriver).
 __device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {

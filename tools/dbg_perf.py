@@ -1,18 +1,35 @@
-"""Protected-GEMM timing under the GG_DEBUG diagnostic switches (one shape)."""
+"""Protected vs unprotected timing of one shape: each arm is a CUDA graph of G launches, and
+the two graphs are replayed alternately R times (both arms see the same clock / power-cap
+state; no host launch overhead).  GG_DEBUG selects the diagnostic switches (read once per
+process).  Usage: dbg_perf.py M N K [R]"""
 import os, sys, torch
 sys.path.insert(0, '.')
 from paper_2310_03841_b200 import kernels as K, _lib as L
 M, N, Kd = [int(v) for v in sys.argv[1:4]]
+R = int(sys.argv[4]) if len(sys.argv) > 4 else 12
+G = int(min(64, max(4, 3e-3 / (2 * M * N * Kd / 1.2e15))))  # ~3 ms of work per graph replay
 x = torch.randn(M, Kd, device='cuda').to(torch.bfloat16); w = (torch.randn(N, Kd, device='cuda') / Kd**.5).to(torch.bfloat16)
 b = torch.zeros(N, device='cuda')
 ws, bs = K.offline_checksum(w, b, L.GG_P_F64); aux = K.checksum_aux(ws, torch.bfloat16); bsv = bs.item()
 y = torch.empty(M, N, dtype=torch.bfloat16, device='cuda'); res = K.CheckResult.empty(M, False, 'cuda')
-def t(fn, iters=30):
-    for _ in range(5): fn()
-    s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize(); s.record()
-    for _ in range(iters): fn()
-    e.record(); torch.cuda.synchronize(); return s.elapsed_time(e) / iters * 1e3
-tu = t(lambda: K.protected_gemm(x, w, b, protect=False, out=y))
-tp = t(lambda: K.protected_gemm(x, w, b, w_sum=ws, w_aux=aux, bias_sum=bsv, lo=-1e30, hi=1e30, out=y, result=res))
-print(f"GG_DEBUG={os.environ.get('GG_DEBUG', '0')} {M}x{N}x{Kd}: unprot {tu:7.1f}us prot {tp:7.1f}us overhead {100*(tp/tu-1):6.1f}%", flush=True)
+unprot = lambda: K.protected_gemm(x, w, b, protect=False, out=y)
+prot = lambda: K.protected_gemm(x, w, b, w_sum=ws, w_aux=aux, bias_sum=bsv, lo=-1e30, hi=1e30, out=y, result=res)
+graphs = []
+for fn in (unprot, prot):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(G): fn()
+    graphs.append(g)
+for g in graphs: g.replay()
+torch.cuda.synchronize()
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * R + 1)]
+ev[0].record()
+for i in range(R):
+    graphs[0].replay(); ev[2 * i + 1].record()
+    graphs[1].replay(); ev[2 * i + 2].record()
+torch.cuda.synchronize()
+tu = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(R)) / (R * G) * 1e3
+tp = sum(ev[2 * i + 1].elapsed_time(ev[2 * i + 2]) for i in range(R)) / (R * G) * 1e3
+print(f"GG_DEBUG={os.environ.get('GG_DEBUG', '0'):>2} {M}x{N}x{Kd}: unprot {tu:7.1f}us prot {tp:7.1f}us overhead {100*(tp/tu-1):6.1f}%  (G={G})", flush=True)

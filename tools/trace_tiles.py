@@ -74,3 +74,15 @@ cu = [t[c, i, 23] for c in range(148) for i in range(TT) if t[c, i, 6] > 0]
 if cw: print('checksum warps per tile (median cycles): wait aready', np.median(cw), 'copy(lds)', np.median(cc), 'fence+arrive', np.median(cm), 'compute', np.median(cu))
 print('median cycles: mma issue', np.median(mma) if mma else None, 'epilogue', np.median(epi) if epi else None,
       'mma wait tempty', np.median(gapt) if gapt else None)
+# tail: per CTA, reducer done minus epilogue done on the CTA's last tile, and per-tile reducer latency
+tails, lat = [], []
+for cta in range(148):
+    r = t[cta]
+    idx = [i for i in range(TT) if r[i, 2] > 0 and r[i, 9] > 0]
+    if not idx: continue
+    i = idx[-1]
+    tails.append(r[i, 9] - r[i, 2])
+    lat += [r[j, 9] - r[j, 8] for j in idx]
+if tails:
+    print('reducer tail after last epilogue (cycles): median', np.median(tails), 'max', np.max(tails),
+          '| reducer per-tile work (got->done): median', np.median(lat), 'p90', np.percentile(lat, 90), 'max', np.max(lat))
