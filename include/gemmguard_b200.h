@@ -70,7 +70,9 @@ enum gg_error {
  * replaces it by `value` rounded to the output type) after bias add and
  * rounding, before the observed checksum — injector.py:265-271 /
  * guard.py:515-523.  target ACCUMULATOR flips the raw fp32/s32 TMEM
- * accumulator before the bias add (build extension). */
+ * accumulator before the bias add (build extension).
+ * An injection list must be sorted by row (ascending; ties in any order):
+ * each epilogue thread binary-searches it once per tile. */
 typedef struct gg_injection {
   int64_t row;
   int32_t col;
@@ -112,7 +114,7 @@ typedef struct gg_gemm_desc {
   int32_t* nflag;             /* scalar: number of flagged rows              */
   uint8_t* triggered;         /* scalar 0/1                                  */
 
-  const gg_injection* inj;    /* device array, may be NULL                   */
+  const gg_injection* inj;    /* device array sorted by row, may be NULL     */
   int32_t n_inj;
 
   void* workspace;            /* zero-filled before first use; every call    */

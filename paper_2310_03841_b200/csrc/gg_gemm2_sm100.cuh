@@ -370,8 +370,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   pair_range(pid, npairs, m_pairs * n_tiles, t0, t1);
   const int hb = min((t0 + n_tiles - 1) / n_tiles * n_tiles, t1);  // end of the leading partial band
   const int tb = max(t1 / n_tiles * n_tiles, hb);                  // start of the trailing partial band
-  const int n_seq = p.sched ? (m_pairs * n_tiles - pid + npairs - 1) / npairs : t1 - t0;
+  // replay: only the listed band pairs (replay_prepare), walked strided
+  const int n_walk = p.replay ? __ldcg(&p.ws.counters[2]) * n_tiles : m_pairs * n_tiles;
+  const int n_seq = p.sched ? max(0, (n_walk - pid + npairs - 1) / npairs) : t1 - t0;
   auto tile_at = [&](int i) -> int {
+    if (p.replay) {
+      const int k = pid + i * npairs;
+      return __ldcg(&p.ws.active_pairs[k / n_tiles]) * n_tiles + k % n_tiles;
+    }
     if (p.sched) return pid + i * npairs;
     if (i < hb - t0) return t0 + i;
     i -= hb - t0;
@@ -698,6 +704,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       float2 obs_a = make_float2(0.f, 0.f), obs_b = make_float2(0.f, 0.f);  // full chunks: pair chains
       long long obs_i = 0;
       int changed = 0;
+      // this row's faults: the list is sorted by row (gg_injection), so one binary search per
+      // tile finds them and each chunk scans only those (a campaign launch carries one per image)
+      int inj_lo = 0, inj_hi = 0;
+      if (p.n_inj > 0 && row_ok) {
+        int a = 0, b = p.n_inj;
+        while (a < b) {
+          const int mid = (a + b) >> 1;
+          if (p.inj[mid].row < row) a = mid + 1;
+          else b = mid;
+        }
+        inj_lo = a;
+        while (b < p.n_inj && p.inj[b].row == row) ++b;
+        inj_hi = b;
+      }
 #ifdef GG_TRACE
       long long tr_ld = 0, tr_cmp = 0, tr_st = 0, tr_obs = 0, tr_t = clock64();
 #define GG_LAP(acc)                 \
@@ -727,9 +747,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         const bool full = (col0 + 32 <= p.N);
         bool out_inj = false;  // an output fault lands in this row's chunk (rare)
-        for (int i = 0; i < p.n_inj; ++i) {
+        for (int i = inj_lo; i < inj_hi; ++i) {
           const gg_injection f = p.inj[i];
-          if (f.row == row && f.col >= col0 && f.col < col0 + 32) {
+          if (f.col >= col0 && f.col < col0 + 32) {
             if (f.target == GG_INJ_ACCUMULATOR) {
 #pragma unroll
               for (int j = 0; j < 32; ++j)  // static indices keep r[] in registers
@@ -764,9 +784,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 32; ++j) o[j] = acc_to_out_bits<OUT>(r[j], bb[j]);
         }
         if (out_inj) {
-          for (int i = 0; i < p.n_inj; ++i) {
+          for (int i = inj_lo; i < inj_hi; ++i) {
             const gg_injection f = p.inj[i];
-            if (f.row != row || f.target != GG_INJ_OUTPUT || f.col < col0 || f.col >= col0 + 32) continue;
+            if (f.target != GG_INJ_OUTPUT || f.col < col0 || f.col >= col0 + 32) continue;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {  // static indices keep o[] in registers
               if (f.col != col0 + j) continue;
@@ -839,6 +859,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           GG_LAP(tr_st);
         } else if (row_ok) {
           const long long base = static_cast<long long>(row) * p.ldc + col0;
+          constexpr int WORDS = OUT16 ? 16 : 32;  // 32-bit words of this row's 32 outputs
+          uint32_t* cw = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(p.C) + base * (OUT16 ? 2 : 4));
+          if (full && (reinterpret_cast<uintptr_t>(cw) & 15) == 0) {
+            // whole chunk: 16-byte loads / stores; replay counts the outputs whose bytes change
+#pragma unroll
+            for (int v = 0; v < WORDS / 4; ++v) {
+              uint4* dst = reinterpret_cast<uint4*>(cw) + v;
+              if (p.replay) {
+                const uint4 old = *dst;
+                const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint32_t nw = o[4 * v + q];
+                  if constexpr (OUT16)
+                    changed += (((ow[q] ^ nw) & 0xFFFFu) != 0) + (((ow[q] ^ nw) >> 16) != 0);
+                  else
+                    changed += ow[q] != nw;
+                }
+              }
+              *dst = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+            }
+            continue;
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (col0 + j >= p.N) continue;

@@ -74,7 +74,7 @@ int num_sms() {
 }
 
 struct WsLayout {
-  size_t summary, counters, band_counter, band_active, band_nflag, band_maxkey, pred, partial, total;
+  size_t summary, counters, band_counter, band_active, active_pairs, band_nflag, band_maxkey, pred, partial, total;
 };
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 WsLayout ws_layout(int64_t M, int64_t N) {
@@ -87,6 +87,7 @@ WsLayout ws_layout(int64_t M, int64_t N) {
   L.counters = off; off = align_up(off + 16, 256);
   L.band_counter = off; off = align_up(off + 4 * m_tiles, 256);
   L.band_active = off; off = align_up(off + m_tiles, 256);
+  L.active_pairs = off; off = align_up(off + 4 * ((m_tiles + 1) / 2), 256);
   L.band_nflag = off; off = align_up(off + 4 * m_tiles, 256);
   L.band_maxkey = off; off = align_up(off + 8 * m_tiles, 256);
   L.pred = off; off = align_up(off + 8 * m_pad * n_tiles, 256);
@@ -99,6 +100,7 @@ WsLayout ws_layout(int64_t M, int64_t N) {
 // inactive bands' standing summaries (the replayed bands add theirs); with no active band
 // the summary is final here.
 __global__ void replay_prepare_kernel(const uint8_t* rows, int M, int m_tiles, uint8_t* band_active, int* counters,
+                                      int* active_pairs,
                                       unsigned long long* summary, const int* band_nflag,
                                       const unsigned long long* band_maxkey, int* changed, int* nflag,
                                       uint8_t* triggered, double* max_disc) {
@@ -126,6 +128,28 @@ __global__ void replay_prepare_kernel(const uint8_t* rows, int M, int m_tiles, u
     }
   }
   __syncthreads();
+  // ascending list of the 256-row band pairs holding an active band (block-wide scan)
+  __shared__ int s_off[1024];
+  const int m_pairs = (m_tiles + 1) / 2;
+  const int per = (m_pairs + blockDim.x - 1) / blockDim.x;
+  const int p0 = min(m_pairs, static_cast<int>(threadIdx.x) * per), p1 = min(m_pairs, p0 + per);
+  int mine = 0;
+  for (int q = p0; q < p1; ++q) mine += (band_active[2 * q] || (2 * q + 1 < m_tiles && band_active[2 * q + 1])) ? 1 : 0;
+  s_off[threadIdx.x] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x); ++i) {
+      const int c = s_off[i];
+      s_off[i] = acc;
+      acc += c;
+    }
+    counters[2] = acc;
+  }
+  __syncthreads();
+  int at = s_off[threadIdx.x];
+  for (int q = p0; q < p1; ++q)
+    if (band_active[2 * q] || (2 * q + 1 < m_tiles && band_active[2 * q + 1])) active_pairs[at++] = q;
   if (threadIdx.x == 0) {
     counters[1] = s_count;
     if (changed) *changed = 0;
@@ -283,6 +307,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
     p.ws.counters = reinterpret_cast<int*>(w + L.counters);
     p.ws.band_counter = reinterpret_cast<int*>(w + L.band_counter);
     p.ws.band_active = w + L.band_active;
+    p.ws.active_pairs = reinterpret_cast<int*>(w + L.active_pairs);
     p.ws.band_nflag = reinterpret_cast<int*>(w + L.band_nflag);
     p.ws.band_maxkey = reinterpret_cast<unsigned long long*>(w + L.band_maxkey);
     p.ws.pred = reinterpret_cast<double*>(w + L.pred);
@@ -290,7 +315,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   }
   if (replay) {
     replay_prepare_kernel<<<1, 1024, 0, s>>>(d->replay_rows, p.M, p.m_tiles, p.ws.band_active, p.ws.counters,
-                                              p.ws.summary, p.ws.band_nflag, p.ws.band_maxkey, d->changed,
+                                              p.ws.active_pairs, p.ws.summary, p.ws.band_nflag, p.ws.band_maxkey, d->changed,
                                               d->nflag, d->triggered, d->max_disc);
     rc = check_launch("replay_prepare");
     if (rc) return rc;
@@ -303,6 +328,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.sched = a_footprint > 40.0e6 ? 1 : 0;
   if (p.dbg & 1024) p.sched = 0;  // diagnostics: force a schedule
   if (p.dbg & 2048) p.sched = 1;
+  if (replay) p.sched = 1;  // replay walks the listed band pairs strided; every band folds via the workspace
 
   switch (kind) {
     case K_BF16:

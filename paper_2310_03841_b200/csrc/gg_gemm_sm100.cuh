@@ -24,7 +24,8 @@ enum : int { O_BF16 = 0, O_F16 = 1, O_F32 = 2, O_I32 = 3 };
 
 struct Workspace {
   unsigned long long* summary;  // [2] {done bands << 32 | flagged rows, max gap key}: one 128-bit CAS per band
-  int* counters;        // [1] active bands (replay)
+  int* counters;        // [1] active 128-row bands, [2] active 256-row band pairs (replay)
+  int* active_pairs;    // [m_pairs] replay: ascending list of the band pairs to recompute
   int* band_counter;    // [m_tiles]
   uint8_t* band_active; // [m_tiles]
   int* band_nflag;      // [m_tiles]

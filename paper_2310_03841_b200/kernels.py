@@ -73,9 +73,11 @@ class Injection:
 
 
 def injections_to_device(injs: Sequence[Injection], device: torch.device) -> torch.Tensor:
+    """Pack injections for the epilogue, sorted by row as the C-ABI requires (stable)."""
     arr = np.zeros(len(injs), dtype=INJ_DTYPE)
     for i, f in enumerate(injs):
         arr[i] = (f.row, f.col, f.bit, f.target, f.mode, f.value)
+    arr = arr[np.argsort(arr["row"], kind="stable")]
     return torch.from_numpy(arr.view(np.uint8).copy()).to(device, non_blocking=False)
 
 
