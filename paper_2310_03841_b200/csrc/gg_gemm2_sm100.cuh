@@ -703,6 +703,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       float obs4[4] = {0.f, 0.f, 0.f, 0.f};  // 16-bit outputs, partial chunks: fp32 chains
       float2 obs_a = make_float2(0.f, 0.f), obs_b = make_float2(0.f, 0.f);  // full chunks: pair chains
       long long obs_i = 0;
+      unsigned obs_ilo = 0u;  // int outputs, full chunks: sums of the low / high 16-bit halves
+      int obs_ihi = 0;
       int changed = 0;
       // this row's faults: the list is sorted by row (gg_injection), so one binary search per
       // tile finds them and each chunk scans only those (a campaign launch carries one per image)
@@ -806,11 +808,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if constexpr (PROTECT) {  // observed row sum of the STORED values (guard.py:170)
           if (row_ok && !(p.dbg & 8)) {
             if constexpr (INT) {
-              long long s = 0;
+              if (full) {
+                // exact: v = hi16 * 2^16 + lo16 (lo unsigned, hi signed); each half summed by one
+                // IDP2A into int32 sums that cannot overflow over this thread's <= 128 outputs
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (full || col0 + j < p.N) s += static_cast<long long>(static_cast<int>(o[j]));
-              obs_i += s;
+                for (int j = 0; j < 32; ++j) {
+                  obs_ilo = __dp2a_lo(o[j], 0x0001u, obs_ilo);                   // + lo16 (unsigned)
+                  obs_ihi = __dp2a_lo(static_cast<int>(o[j]), 0x0100, obs_ihi);  // + hi16 (signed)
+                }
+              } else {
+                long long s = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (col0 + j < p.N) s += static_cast<long long>(static_cast<int>(o[j]));
+                obs_i += s;
+              }
             } else if constexpr (OUT == O_F32) {
               double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -925,7 +937,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         mbar_wait(&oempty_bar[slot], (static_cast<uint32_t>(local / NSLOT) & 1u) ^ 1u);
         if (lead) GG_EV(3, local);
         const int io = (2 * slot + half) * BM + tid;
-        if constexpr (INT) reinterpret_cast<long long*>(slot_obs)[io] = obs_i;
+        if constexpr (INT)
+          reinterpret_cast<long long*>(slot_obs)[io] =
+              obs_i + static_cast<long long>(obs_ihi) * 65536ll + static_cast<long long>(obs_ilo);
         else if constexpr (OUT16) reinterpret_cast<float2*>(slot_obs)[io] = make_float2(obs_hi, obs_lo);
         else slot_obs[io] = obs;
         __syncwarp();
