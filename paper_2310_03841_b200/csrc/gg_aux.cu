@@ -109,27 +109,89 @@ __device__ __forceinline__ void store_acc<AccI64>(void* out, int64_t i, long lon
 // ------------------------------------------------------------ K2 offline checksum
 // w_sum[k] = fold_n W(k, n); W(k, n) = layout 0: W[n*ldw + k] (torch [N,K]);
 // layout 1: Wt[k*ldw + n] (reference [K,N]).
-template <class A>
-__global__ void offline_checksum_kernel(int w_dtype, const void* W, int64_t K, int64_t N, int64_t ldw, int layout,
-                                        void* w_sum) {
+// One thread per k folds n = 0..N-1 in ascending order (bit-exact with the
+// reference's fold); the source dtype is a template constant and the loads of 32
+// rows are issued ahead of their adds, so the kernel runs at memory-level
+// parallelism instead of one dependent load per add.
+template <class A, int DT>
+__global__ void __launch_bounds__(64) offline_checksum_kernel(const void* W, int64_t K, int64_t N, int64_t ldw,
+                                                             int layout, void* w_sum) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= K) return;
   auto idx = [&](int64_t n) { return layout == 0 ? n * ldw + k : k * ldw + n; };
-  typename A::T acc = A::from(W, w_dtype, idx(0));
-  for (int64_t n = 1; n < N; ++n) acc = A::add(acc, A::from(W, w_dtype, idx(n)));
+  using T = typename A::T;
+  T acc = A::from(W, DT, idx(0));
+  constexpr int U = 32;
+  int64_t n = 1;
+  for (; n + U <= N; n += U) {
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = A::from(W, DT, idx(n + u));
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = A::add(acc, v[u]);
+  }
+  for (; n < N; ++n) acc = A::add(acc, A::from(W, DT, idx(n)));
   store_acc<A>(w_sum, k, acc);
 }
 template <class A>
-__global__ void vector_sum_kernel(int dtype, const void* v, int64_t n, void* out) {
+int launch_k2(int w_dtype, const void* W, int64_t K, int64_t N, int64_t ldw, int layout, void* w_sum, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>((K + 63) / 64);
+  switch (w_dtype) {
+#define GG_K2_CASE(DTV)                                                                         \
+  case DTV:                                                                                     \
+    offline_checksum_kernel<A, DTV><<<g, 64, 0, s>>>(W, K, N, ldw, layout, w_sum);           \
+    return 0;
+    GG_K2_CASE(GG_F64)
+    GG_K2_CASE(GG_F32)
+    GG_K2_CASE(GG_F16)
+    GG_K2_CASE(GG_BF16)
+    GG_K2_CASE(GG_I8)
+    GG_K2_CASE(GG_I32)
+    GG_K2_CASE(GG_I64)
+#undef GG_K2_CASE
+  }
+  return fail(GG_EINVAL, "offline_checksum: bad weight dtype");
+}
+// bias_sum = fold_n bias[n] (ascending, one thread; loads issued 32 ahead of the adds)
+template <class A, int DT>
+__global__ void vector_sum_kernel(const void* v, int64_t n, void* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  typename A::T acc;
+  using T = typename A::T;
+  T acc;
   if (v == nullptr || n == 0) {
-    acc = typename A::T(0);
+    acc = T(0);
   } else {
-    acc = A::from(v, dtype, 0);
-    for (int64_t i = 1; i < n; ++i) acc = A::add(acc, A::from(v, dtype, i));
+    acc = A::from(v, DT, 0);
+    constexpr int U = 32;
+    int64_t i = 1;
+    for (; i + U <= n; i += U) {
+      T x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = A::from(v, DT, i + u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = A::add(acc, x[u]);
+    }
+    for (; i < n; ++i) acc = A::add(acc, A::from(v, DT, i));
   }
   store_acc<A>(out, 0, acc);
+}
+template <class A>
+void launch_vector_sum(int dtype, const void* v, int64_t n, void* out, cudaStream_t s) {
+  switch (dtype) {
+#define GG_VS_CASE(DTV)                                            \
+  case DTV:                                                        \
+    vector_sum_kernel<A, DTV><<<1, 32, 0, s>>>(v, n, out);         \
+    return;
+    GG_VS_CASE(GG_F64)
+    GG_VS_CASE(GG_F32)
+    GG_VS_CASE(GG_F16)
+    GG_VS_CASE(GG_BF16)
+    GG_VS_CASE(GG_I8)
+    GG_VS_CASE(GG_I32)
+    GG_VS_CASE(GG_I64)
+#undef GG_VS_CASE
+  }
+  vector_sum_kernel<A, GG_F64><<<1, 32, 0, s>>>(nullptr, 0, out);  // no bias: sum 0
 }
 
 // ------------------------------------------------------------ verify (exact)
@@ -421,23 +483,22 @@ int launch_offline_checksum(int w_dtype, const void* W, int64_t K, int64_t N, in
   if (!w_int && chk_prec == GG_P_I64) return fail(GG_EINVAL, "int64-exact checksums only apply to integer layers");
   if (K < 1 || N < 1) return fail(GG_EINVAL, "offline_checksum: empty weight");
   if (dtype_bytes(w_dtype) == 0) return fail(GG_EINVAL, "offline_checksum: bad weight dtype");
-  const unsigned g = grid1(K, 256);
   switch (chk_prec) {
     case GG_P_F64:
-      offline_checksum_kernel<AccF64><<<g, 256, 0, s>>>(w_dtype, W, K, N, ldw, w_layout, w_sum_out);
-      vector_sum_kernel<AccF64><<<1, 32, 0, s>>>(bias_dtype, bias, N, bias_sum_out);
+      if (int rc = launch_k2<AccF64>(w_dtype, W, K, N, ldw, w_layout, w_sum_out, s)) return rc;
+      launch_vector_sum<AccF64>(bias_dtype, bias, N, bias_sum_out, s);
       break;
     case GG_P_F32:
-      offline_checksum_kernel<AccF32><<<g, 256, 0, s>>>(w_dtype, W, K, N, ldw, w_layout, w_sum_out);
-      vector_sum_kernel<AccF32><<<1, 32, 0, s>>>(bias_dtype, bias, N, bias_sum_out);
+      if (int rc = launch_k2<AccF32>(w_dtype, W, K, N, ldw, w_layout, w_sum_out, s)) return rc;
+      launch_vector_sum<AccF32>(bias_dtype, bias, N, bias_sum_out, s);
       break;
     case GG_P_F16:
-      offline_checksum_kernel<AccF16><<<g, 256, 0, s>>>(w_dtype, W, K, N, ldw, w_layout, w_sum_out);
-      vector_sum_kernel<AccF16><<<1, 32, 0, s>>>(bias_dtype, bias, N, bias_sum_out);
+      if (int rc = launch_k2<AccF16>(w_dtype, W, K, N, ldw, w_layout, w_sum_out, s)) return rc;
+      launch_vector_sum<AccF16>(bias_dtype, bias, N, bias_sum_out, s);
       break;
     case GG_P_I64:
-      offline_checksum_kernel<AccI64><<<g, 256, 0, s>>>(w_dtype, W, K, N, ldw, w_layout, w_sum_out);
-      vector_sum_kernel<AccI64><<<1, 32, 0, s>>>(bias_dtype, bias, N, bias_sum_out);
+      if (int rc = launch_k2<AccI64>(w_dtype, W, K, N, ldw, w_layout, w_sum_out, s)) return rc;
+      launch_vector_sum<AccI64>(bias_dtype, bias, N, bias_sum_out, s);
       break;
     default:
       return fail(GG_EINVAL, "offline_checksum: unknown precision");
