@@ -49,7 +49,7 @@ namespace pair {
 // device buffer (gg_trace_buffer); compiled out of the production library.
 #ifdef GG_TRACE
 __device__ unsigned long long* g_trace = nullptr;
-constexpr int TRACE_TILES = 64, TRACE_EV = 24;
+constexpr int TRACE_TILES = 64, TRACE_EV = 28;
 #define GG_EV(ev, local)                                                                                  \
   do {                                                                                                  \
     if (g_trace != nullptr && (local) < TRACE_TILES)                                                    \
@@ -98,6 +98,9 @@ __device__ __forceinline__ void pair_range(int pid, int npairs, int total, int& 
 template <bool INT>
 __device__ void finish_band(const Params& p, int mb, int lane, const double (&obs_f)[4], const double (&pred_f)[4],
                             const long long (&obs_i)[4], const long long (&pred_i)[4]) {
+#ifdef GG_TRACE
+  const long long fb_t0 = clock64();
+#endif
   const bool per_sample = INT || p.statistic == GG_PER_SAMPLE;
   const bool bmean = !INT && p.statistic == GG_BATCH_MEAN;
   int nflag = 0;
@@ -146,6 +149,9 @@ __device__ void finish_band(const Params& p, int mb, int lane, const double (&ob
       p.ws.band_maxkey[mb] = key;
     }
   };
+#ifdef GG_TRACE
+  const long long fb_t1 = clock64();
+#endif
   // Launch summary: atomicMax of the band's gap key, then a release-add of
   // {1 << 32 | flagged rows}; the band that completes the count acquires and reads the
   // totals.  The release has no outstanding stores to wait for when the rows are stored
@@ -168,7 +174,19 @@ __device__ void finish_band(const Params& p, int mb, int lane, const double (&ob
       fin_key = atomicMax(&p.ws.summary[1], 0ull);
     }
   }
+#ifdef GG_TRACE
+  const long long fb_t2 = clock64();
+#endif
   if (!bmean) store_rows();
+#ifdef GG_TRACE
+  if (lane == 0 && g_trace != nullptr) {
+    const size_t b = static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV;
+    g_trace[b + 24] = fb_t0;
+    g_trace[b + 25] = fb_t1;
+    g_trace[b + 26] = fb_t2;
+    g_trace[b + 27] = clock64();
+  }
+#endif
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
   int nf = static_cast<int>(__shfl_sync(0xffffffffu, fin_rows, 0));
@@ -604,8 +622,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         if (band_ok) {
           if (whole) {
-            if (n == n_tiles - 1) finish(mb, ao, ap);
-          } else if (p.sched || t == min((m + 1) * n_tiles, t1) - 1) {
+            if (n == n_tiles - 1 && !(p.dbg & 64)) finish(mb, ao, ap);
+          } else if ((p.sched || t == min((m + 1) * n_tiles, t1) - 1) && !(p.dbg & 128)) {
             // the pair's last tile of this band: release its partials with one count of the
             // tiles it contributed (contiguous schedule: at most two such parts per pair)
             const int part = p.sched ? 1 : min((m + 1) * n_tiles, t1) - max(m * n_tiles, t0);

@@ -61,7 +61,8 @@ struct Params {
   int sched;            // 0: contiguous tile range per pair, 1: strided (long K)
   int dbg;              // diagnostics only ($GG_DEBUG), 0 in production: 1 skip predicted dot products,
                         // 2 decouple the checksum warps from the stages, 4 skip band folds, 8 skip
-                        // observed sums, 1024 / 2048 force the contiguous / strided schedule
+                        // observed sums, 64 skip local band finishes, 128 skip split-band exchanges,
+                        // 1024 / 2048 force the contiguous / strided schedule
   int replay;           // 1: only active bands, compare against old C
   int* changed;
   Workspace ws;

@@ -1,0 +1,16 @@
+# Locked-clock (ncu base clocks) A/B of library variants: per-launch kernel durations of
+# tools/prof_one.py (2 unprotected + 2 protected launches) per shape.
+# usage: bash tools/ab_ncu.sh "M N K" variant...   (variant "cur" = the in-tree library)
+shape=$1; shift
+for v in "$@"; do
+  if [ "$v" != cur ]; then export GEMMGUARD_LIB=paper_2310_03841_b200/_build/libgemmguard_b200_$v.so; else unset GEMMGUARD_LIB; fi
+  ncu --metrics gpu__time_duration.sum -k regex:gg_protected --csv python tools/prof_one.py $shape bf16 2>/dev/null \
+    | python -c "
+import sys, csv
+rows = list(csv.reader(sys.stdin)); h = next(r for r in rows if 'Kernel Name' in r); K = h.index('Kernel Name'); V = h.index('Metric Value')
+u = [float(r[V].replace(',', '')) for r in rows[rows.index(h) + 1:] if len(r) == len(h) and r[K].rstrip().endswith('0>(CUtensorMap_st, CUtensorMap_st, CUtensorMap_st, Params)')]
+p = [float(r[V].replace(',', '')) for r in rows[rows.index(h) + 1:] if len(r) == len(h) and r[K].rstrip().endswith('1>(CUtensorMap_st, CUtensorMap_st, CUtensorMap_st, Params)')]
+print(f'[$v] $shape unprot {sum(u)/len(u)/1e3:.1f}us prot {sum(p)/len(p)/1e3:.1f}us overhead {100*(sum(p)/len(p)/(sum(u)/len(u))-1):.1f}%')
+"
+done
+unset GEMMGUARD_LIB

@@ -15,7 +15,7 @@ b = torch.zeros(N, device='cuda')
 ws, bs = K.offline_checksum(w, b, L.GG_P_F64); aux = K.checksum_aux(ws, torch.bfloat16); bsv = bs.item()
 y = torch.empty(M, N, dtype=torch.bfloat16, device='cuda'); res = K.CheckResult.empty(M, False, 'cuda')
 lib = L.load(); lib.gg_trace_buffer.argtypes = [ctypes.c_void_p]
-TT, EV = 64, 24
+TT, EV = 64, 28
 buf = torch.zeros(148 * TT * EV + 4 * 64 * 4, dtype=torch.int64, device='cuda')
 run = (lambda: K.protected_gemm(x, w, b, w_sum=ws, w_aux=aux, bias_sum=bsv, lo=-1e30, hi=1e30, out=y, result=res)) \
     if protect else (lambda: K.protected_gemm(x, w, b, protect=False, out=y))
@@ -86,3 +86,10 @@ for cta in range(148):
 if tails:
     print('reducer tail after last epilogue (cycles): median', np.median(tails), 'max', np.max(tails),
           '| reducer per-tile work (got->done): median', np.median(lat), 'p90', np.percentile(lat, 90), 'max', np.max(lat))
+
+# last band finish of each CTA (overwritten per finish): compute / atomics / stores
+fc = [(t[c, 0, 25] - t[c, 0, 24], t[c, 0, 26] - t[c, 0, 25], t[c, 0, 27] - t[c, 0, 26]) for c in range(148) if t[c, 0, 24] > 0]
+if fc:
+    a = np.array(fc)
+    print('last band finish (median cycles): d/flags compute', np.median(a[:, 0]), 'summary atomics', np.median(a[:, 1]),
+          'row stores', np.median(a[:, 2]))
