@@ -475,7 +475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           tr_empty += tw1 - tw0;
 #endif
           if ((chk_pending & (1u << stage)) && !(p.dbg & 2)) {  // the checksum warps still hold the stage's previous K-block
-            mbar_wait_spin(&chkdone_bar[stage], (chk_phase >> stage) & 1u);
+            mbar_wait(&chkdone_bar[stage], (chk_phase >> stage) & 1u);
 #ifdef GG_TRACE
             tr_chk += clock64() - tw1;
 #endif
@@ -1001,7 +1001,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 8; ++j) v[j] = make_uint4(kb, s, tid, 0);
           return;
         }
-        mbar_wait_spin(&aready_bar[s], (ar_phase >> s) & 1u);
+        mbar_wait(&aready_bar[s], (ar_phase >> s) & 1u);  // suspending wait: equal latency, no spin
         ar_phase ^= 1u << s;
 #ifdef GG_TRACE
         const long long c1 = clock64();
