@@ -213,20 +213,18 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         else:
             K.protected_gemm(ly["x"], ly["w"], ly["b"], protect=False, out=ly["y"])
 
-    # ---- per-layer epsilon: two clean calibration batches (fresh activations each)
-    ds = {ly["name"]: [] for ly in layers}
+    # ---- per-layer epsilon: two clean calibration batches (fresh activations each); the
+    # fused check's d is folded into device-resident running moments (calib.RunningStats)
+    from paper_2310_03841_b200 import calib
+    stats = {ly["name"]: calib.RunningStats(dev) for ly in layers}
     for c in range(2):
         for ly in layers:
             if c:
                 ly["x"].copy_(torch.randn(ly["M"], ly["K"], device=dev, generator=g).to(torch.bfloat16))
             launch(ly)
-            ds[ly["name"]].append(ly["res"].d.clone())
-    torch.cuda.synchronize()
+            stats[ly["name"]].update(ly["res"].d)
     for ly in layers:
-        d = torch.cat(ds[ly["name"]]).double().cpu().numpy()
-        mu, sd = float(d.mean()), float(d.std(ddof=1))
-        z = statistics.NormalDist().inv_cdf((1 + CONFIDENCE) / 2)
-        ly["mu"], ly["lo"], ly["hi"] = mu, mu - z * sd, mu + z * sd
+        ly["mu"], ly["lo"], ly["hi"] = stats[ly["name"]].epsilon(CONFIDENCE)
         ly["x"].copy_(torch.randn(ly["M"], ly["K"], device=dev, generator=g).to(torch.bfloat16))  # held-out
 
     # ---- capture one step (50 launches) as a CUDA graph, protected and unprotected

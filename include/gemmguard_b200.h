@@ -211,6 +211,21 @@ GG_API int gg_reduce(int32_t dtype, const void* A, int64_t rows, int64_t cols,
 GG_API int gg_round_f64_to(int32_t dtype, const double* in, void* out, int64_t n,
                     void* stream); /* RNE: numerics._round_array 202-208 */
 
+/* Calibration statistics (guard.calibrate_epsilon, guard.py:300-355): merge
+ * the n discrepancies d[0..n) (f64, device) into the device-resident running
+ * state[3] = {count, mean, M2} (Welford per chunk, Chan's pairwise merge over
+ * a fixed tree: deterministic).  sigma = sqrt(M2 / (count - 1)). Zero the
+ * state before the first batch. */
+GG_API int gg_running_stats(const double* d, int64_t n, double* state, void* stream);
+
+/* Range profiling (profiler.profile_ranges, profiler.py:62-80): update the
+ * running state[3] = {key(min), key(max), non-finite count} with the finite
+ * values of Y [M, N] (row pitch ldy elements; dtype GG_BF16, GG_F16, GG_F32 or
+ * GG_I32).  key(v) maps a double onto uint64 preserving order: bits | 2^63
+ * for v >= 0, ~bits for v < 0.  Initialise state to {~0, 0, 0}. */
+GG_API int gg_minmax(int32_t dtype, const void* Y, int64_t M, int64_t N, int64_t ldy,
+                     uint64_t* state, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

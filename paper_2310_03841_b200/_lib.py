@@ -40,6 +40,8 @@ EXPORTED_SYMBOLS = (
     "gg_gemm_exact",
     "gg_reduce",
     "gg_round_f64_to",
+    "gg_running_stats",
+    "gg_minmax",
 )
 
 
@@ -144,6 +146,10 @@ def load(path: Path | None = None):
                                   c_void_p, c_void_p]
     lib.gg_reduce.restype = c_int32
     lib.gg_reduce.argtypes = [c_int32, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p]
+    lib.gg_running_stats.restype = c_int32
+    lib.gg_running_stats.argtypes = [c_void_p, c_int64, c_void_p, c_void_p]
+    lib.gg_minmax.restype = c_int32
+    lib.gg_minmax.argtypes = [c_int32, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]
     lib.gg_round_f64_to.restype = c_int32
     lib.gg_round_f64_to.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p]
     _lib = lib

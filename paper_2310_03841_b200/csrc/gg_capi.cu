@@ -84,4 +84,13 @@ int gg_round_f64_to(int32_t dtype, const double* in, void* out, int64_t n, void*
   return gg::launch_round(dtype, in, out, n, static_cast<cudaStream_t>(stream));
 }
 
+int gg_running_stats(const double* d, int64_t n, double* state, void* stream) {
+  return gg::launch_running_stats(d, n, state, static_cast<cudaStream_t>(stream));
+}
+
+int gg_minmax(int32_t dtype, const void* Y, int64_t M, int64_t N, int64_t ldy, uint64_t* state, void* stream) {
+  return gg::launch_minmax(dtype, Y, M, N, ldy, reinterpret_cast<unsigned long long*>(state),
+                           static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

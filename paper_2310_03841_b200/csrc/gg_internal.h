@@ -50,6 +50,11 @@ int launch_round(int dtype, const double* in, void* out, int64_t n, cudaStream_t
 size_t checksum_aux_bytes(int ab_kind, int64_t K);
 int launch_checksum_aux(int ab_kind, const void* w_sum, int64_t K, void* aux, cudaStream_t s);
 
+// implemented in gg_calib.cu
+int launch_running_stats(const double* d, int64_t n, double* state, cudaStream_t s);
+int launch_minmax(int dtype, const void* Y, int64_t M, int64_t N, int64_t ldy, unsigned long long* state,
+                  cudaStream_t s);
+
 // implemented in gg_gemm_sm100.cu
 size_t protected_gemm_workspace_bytes(int64_t M, int64_t N);
 int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s);

@@ -378,9 +378,26 @@ def run_cfg5(out):
           "target_pct": 2.0}, out)
 
 
+# ---------------------------------------------------------------- calibration kernels (§8(f) 1)
+def run_calib(out):
+    from paper_2310_03841_b200 import calib
+    hbm = json.load(open("MEASURED_PEAKS.json")).get("hbm_gbs", 6548.5) if __import__("os").path.exists(
+        "MEASURED_PEAKS.json") else 6548.5
+    d = torch.randn(50432, device=DEV, dtype=torch.float64)
+    st = calib.RunningStats(DEV)
+    (t_stats,) = interleaved([lambda: st.update(d)], 50, rounds=4)
+    y = torch.randn(50432, 3072, device=DEV).to(torch.bfloat16)
+    rr = calib.RunningRange(DEV)
+    (t_mm,) = interleaved([lambda: rr.update(y)], 20, rounds=4)
+    gbs = y.numel() * 2 / (t_mm * 1e-6) / 1e9
+    emit({"config": "calib", "scope": "device calibration kernels: running (n, mean, M2) of one ViT-B layer's d "
+          "(50432 rows) and running min / max of a fc1 output (50432 x 3072 bf16)",
+          "us_running_stats": t_stats, "us_minmax": t_mm, "minmax_gbs": gbs, "minmax_frac_of_hbm": gbs / hbm}, out)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="peaks,cfg1,cfg2,cfg4,cfg5")
+    ap.add_argument("--only", default="peaks,cfg1,cfg2,cfg4,cfg5,calib")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     sel = a.only.split(",")
@@ -395,6 +412,8 @@ def main():
         run_cfg4(a.out, "tf32")
     if "cfg5" in sel:
         run_cfg5(a.out)
+    if "calib" in sel:
+        run_calib(a.out)
 
 
 if __name__ == "__main__":
