@@ -226,6 +226,15 @@ GG_API int gg_running_stats(const double* d, int64_t n, double* state, void* str
 GG_API int gg_minmax(int32_t dtype, const void* Y, int64_t M, int64_t N, int64_t ldy,
                      uint64_t* state, void* stream);
 
+/* Integer toy-pipeline glue (model.finish_layer_output for integer models,
+ * model.py:307-331), batched: Y [B*T, N] int32 raw GEMM outputs (row pitch ldy)
+ * -> H int8 hidden state.  relu (mlp_fc1) then requantise
+ * clip((h + 2^(shift-1)) >> shift, -128, 127); for qkv layers (qkv != 0) also
+ * the head mix floor((q+k+v)/3) and token mix floor((m + floor(sum_t m / T)) / 2)
+ * per sample, giving H [B*T, N/3].  NumPy integer semantics: bit-exact. */
+GG_API int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int64_t ldy,
+                         int32_t relu, int32_t shift, int32_t qkv, int8_t* H, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

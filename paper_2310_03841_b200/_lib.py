@@ -42,6 +42,7 @@ EXPORTED_SYMBOLS = (
     "gg_round_f64_to",
     "gg_running_stats",
     "gg_minmax",
+    "gg_int_finish",
 )
 
 
@@ -150,6 +151,9 @@ def load(path: Path | None = None):
     lib.gg_running_stats.argtypes = [c_void_p, c_int64, c_void_p, c_void_p]
     lib.gg_minmax.restype = c_int32
     lib.gg_minmax.argtypes = [c_int32, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]
+    lib.gg_int_finish.restype = c_int32
+    lib.gg_int_finish.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32, c_void_p,
+                                  c_void_p]
     lib.gg_round_f64_to.restype = c_int32
     lib.gg_round_f64_to.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p]
     _lib = lib

@@ -93,4 +93,9 @@ int gg_minmax(int32_t dtype, const void* Y, int64_t M, int64_t N, int64_t ldy, u
                            static_cast<cudaStream_t>(stream));
 }
 
+int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int64_t ldy, int32_t relu, int32_t shift,
+                  int32_t qkv, int8_t* H, void* stream) {
+  return gg::launch_int_finish(Y, B, T, N, ldy, relu, shift, qkv, H, static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

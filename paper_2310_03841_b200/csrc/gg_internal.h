@@ -55,6 +55,10 @@ int launch_running_stats(const double* d, int64_t n, double* state, cudaStream_t
 int launch_minmax(int dtype, const void* Y, int64_t M, int64_t N, int64_t ldy, unsigned long long* state,
                   cudaStream_t s);
 
+// implemented in gg_toy.cu
+int launch_int_finish(const int* y, int64_t B, int64_t T, int64_t N, int64_t ldy, int relu, int shift, int qkv,
+                      int8_t* h, cudaStream_t s);
+
 // implemented in gg_gemm_sm100.cu
 size_t protected_gemm_workspace_bytes(int64_t M, int64_t N);
 int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s);

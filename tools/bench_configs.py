@@ -395,9 +395,34 @@ def run_calib(out):
           "us_running_stats": t_stats, "us_minmax": t_mm, "minmax_gbs": gbs, "minmax_frac_of_hbm": gbs / hbm}, out)
 
 
+# ---------------------------------------------------------------- int8 toy on the device (§8(f) 2)
+def run_toy_int8(out):
+    from paper_2310_03841_b200 import model as Mo
+    from paper_2310_03841_b200 import toy_device as TD
+    from paper_2310_03841_b200.numerics import Matrix2D
+    model = Mo.build_toy_model(12, 768, 197, 1000, 0, "int8")
+    rng = np.random.default_rng(1)
+    inputs = [Matrix2D(rng.integers(-31, 32, (197, 768)), "int8") for _ in range(64)]
+    TD.forward_batch(model, inputs[:4], protect=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    outb = TD.forward_batch(model, inputs, protect=True)
+    t_batch = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ref = Mo.forward(model, inputs[0], 0)
+    t_host = time.perf_counter() - t0
+    same = outb.logits[0].tolist() == ref.logits.tolist()
+    emit({"config": "toy_int8_device", "scope": "integer toy with ViT-B dims (12 blocks, dim 768, 197 tokens, "
+          "1000 classes; token mixing stands in for attention): batched device forward, every GEMM protected "
+          "(int64-exact), host inputs in / logits out", "batch": len(inputs),
+          "images_per_s_device_batch": len(inputs) / t_batch, "s_per_image_host_glue": t_host,
+          "logits_identical_to_host_path": same, "flags_clean": all(not f.any() for f in outb.flagged.values()),
+          "cpu_reference_s_per_image_BASELINE_md": 12.0}, out)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="peaks,cfg1,cfg2,cfg4,cfg5,calib")
+    ap.add_argument("--only", default="peaks,cfg1,cfg2,cfg4,cfg5,calib,toy")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     sel = a.only.split(",")
@@ -414,6 +439,8 @@ def main():
         run_cfg5(a.out)
     if "calib" in sel:
         run_calib(a.out)
+    if "toy" in sel:
+        run_toy_int8(a.out)
 
 
 if __name__ == "__main__":
