@@ -321,26 +321,47 @@ def measure_e2e(layers, launch, dev, args, world):
     host_flags = torch.empty(len(layers), dtype=torch.int32).pin_memory()
     flops = gemm_flops([(ly["name"], ly["M"], ly["N"], ly["K"]) for ly in layers])
 
-    def step():
-        first["x"].copy_(host_x, non_blocking=True)
+    # the next step's input batch is copied on a side stream while this step computes
+    # (double-buffered layer-0 input); every step still moves its whole batch from pinned
+    # host memory and the host consumes flags + logits before the next step
+    x_bufs = [first["x"], torch.empty_like(first["x"])]
+    copy_stream = torch.cuda.Stream(dev)
+    compute = torch.cuda.current_stream(dev)
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def prefetch(i):
+        copy_stream.wait_stream(compute)  # the buffer's previous reader (step i - 2) has finished
+        with torch.cuda.stream(copy_stream):
+            x_bufs[i % 2].copy_(host_x, non_blocking=True)
+            copied[i % 2].record(copy_stream)
+
+    def step(i):
+        compute.wait_event(copied[i % 2])
+        first["x"] = x_bufs[i % 2]
+        prefetch(i + 1)  # always: the timed region holds exactly one full batch copy per step
         for ly in layers:
             launch(ly)
         host_flags.copy_(torch.cat([ly["res"].nflag for ly in layers]), non_blocking=True)
         host_logits.copy_(head["y"], non_blocking=True)
 
-    for _ in range(args.warmup):
-        step()
+    n_total = args.warmup + args.steps
+    prefetch(0)
+    for i in range(args.warmup):
+        step(i)
+        compute.synchronize()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    for _ in range(args.steps):
-        step()
-        torch.cuda.current_stream().synchronize()  # the host consumes flags + logits every step
+    for i in range(args.warmup, n_total):
+        step(i)
+        compute.synchronize()  # the host consumes flags + logits every step
+    compute.wait_stream(copy_stream)
     ev1.record()
     torch.cuda.synchronize()
+    first["x"] = x_bufs[0]
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
