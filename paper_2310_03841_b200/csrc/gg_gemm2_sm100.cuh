@@ -92,106 +92,77 @@ __device__ __forceinline__ void pair_range(int pid, int npairs, int total, int& 
   t1 = static_cast<int>(static_cast<long long>(pid + 1) * total / npairs);
 }
 
-// d / flags of the rows lane + 32q (q < 4) of band mb from their folded sums,
-// then the band summary and, for the last band of the launch, the launch
-// summaries (nflag, triggered, max_disc).  One warp.
+// d / flags of the rows lane + 32q (q < 4) of band mb from their folded sums, with the
+// band's flag count and largest gap key reduced over the warp (no stores).
 template <bool INT>
-__device__ void finish_band(const Params& p, int mb, int lane, const double (&obs_f)[4], const double (&pred_f)[4],
-                            const long long (&obs_i)[4], const long long (&pred_i)[4]) {
-#ifdef GG_TRACE
-  const long long fb_t0 = clock64();
-#endif
-  const bool per_sample = INT || p.statistic == GG_PER_SAMPLE;
-  const bool bmean = !INT && p.statistic == GG_BATCH_MEAN;
-  int nflag = 0;
-  unsigned long long key = 0;
-  unsigned long long dbits[4];  // d of rows lane + 32q (f64 or i64 bits)
+struct BandRows {
+  unsigned long long dbits[4];  // d (f64 or i64 bits)
   bool flag[4];
+  int nflag;
+  unsigned long long key;
+};
+
+template <bool INT>
+__device__ __forceinline__ BandRows<INT> band_rows(const Params& p, int mb, int lane, const double (&obs_f)[4],
+                                                  const double (&pred_f)[4], const long long (&obs_i)[4],
+                                                  const long long (&pred_i)[4]) {
+  const bool per_sample = INT || p.statistic == GG_PER_SAMPLE;
+  BandRows<INT> r;
+  r.nflag = 0;
+  r.key = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int row = mb * BM + lane + 32 * q;
-    flag[q] = false;
-    dbits[q] = 0;
+    r.flag[q] = false;
+    r.dbits[q] = 0;
     if (row >= p.M) continue;
     if constexpr (INT) {
       const long long di = (pred_i[q] + p.bias_sum_i) - obs_i[q];
-      dbits[q] = static_cast<unsigned long long>(di);
-      flag[q] = di != 0;
+      r.dbits[q] = static_cast<unsigned long long>(di);
+      r.flag[q] = di != 0;
       const unsigned long long mag =
           di < 0 ? 0ull - static_cast<unsigned long long>(di) : static_cast<unsigned long long>(di);
       const unsigned long long k = gap_key(static_cast<double>(mag));
-      key = k > key ? k : key;
+      r.key = k > r.key ? k : r.key;
     } else {
       const double dd = (pred_f[q] + p.bias_sum_f) - obs_f[q];
-      dbits[q] = static_cast<unsigned long long>(__double_as_longlong(dd));
-      flag[q] = !((dd >= p.lo) && (dd <= p.hi));
+      r.dbits[q] = static_cast<unsigned long long>(__double_as_longlong(dd));
+      r.flag[q] = !((dd >= p.lo) && (dd <= p.hi));
       const unsigned long long k = gap_key(fabs(dd - p.mu));
-      key = k > key ? k : key;
+      r.key = k > r.key ? k : r.key;
     }
-    if (per_sample) nflag += flag[q] ? 1 : 0;
+    if (per_sample) r.nflag += r.flag[q] ? 1 : 0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    nflag += __shfl_xor_sync(0xffffffffu, nflag, o);
-    const unsigned long long w = __shfl_xor_sync(0xffffffffu, key, o);
-    key = w > key ? w : key;
+    r.nflag += __shfl_xor_sync(0xffffffffu, r.nflag, o);
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, r.key, o);
+    r.key = w > r.key ? w : r.key;
   }
-  auto store_rows = [&]() {
+  return r;
+}
+
+// Row stores (d, per-sample flags) and the band summary of band_rows' result.
+template <bool INT>
+__device__ __forceinline__ void store_band(const Params& p, int mb, int lane, const BandRows<INT>& r) {
+  const bool per_sample = INT || p.statistic == GG_PER_SAMPLE;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int row = mb * BM + lane + 32 * q;
-      if (row >= p.M) continue;
-      static_cast<unsigned long long*>(p.d)[row] = dbits[q];
-      if (per_sample) p.flags[row] = flag[q] ? 1 : 0;
-    }
-    if (lane == 0) {
-      p.ws.band_nflag[mb] = nflag;
-      p.ws.band_maxkey[mb] = key;
-    }
-  };
-#ifdef GG_TRACE
-  const long long fb_t1 = clock64();
-#endif
-  // Launch summary: atomicMax of the band's gap key, then a release-add of
-  // {1 << 32 | flagged rows}; the band that completes the count acquires and reads the
-  // totals.  The release has no outstanding stores to wait for when the rows are stored
-  // after it (the batch-mean statistic reads every row's d, so there they go first).
-  if (bmean) {
-    store_rows();
-    __syncwarp();
+  for (int q = 0; q < 4; ++q) {
+    const int row = mb * BM + lane + 32 * q;
+    if (row >= p.M) continue;
+    static_cast<unsigned long long*>(p.d)[row] = r.dbits[q];
+    if (per_sample) p.flags[row] = r.flag[q] ? 1 : 0;
   }
-  int last = 0;
-  unsigned long long fin_rows = 0, fin_key = 0;
   if (lane == 0) {
-    const int total = p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles;
-    atomicMax(&p.ws.summary[1], key);
-    const unsigned long long inc = (1ull << 32) | static_cast<unsigned>(nflag);
-    const unsigned long long old = atom_add_release_gpu_u64(&p.ws.summary[0], inc);
-    last = (static_cast<long long>(old >> 32) + 1 == total) ? 1 : 0;
-    if (last) {
-      fence_acquire_gpu();
-      fin_rows = (old + inc) & 0xFFFFFFFFull;
-      fin_key = atomicMax(&p.ws.summary[1], 0ull);
-    }
+    p.ws.band_nflag[mb] = r.nflag;
+    p.ws.band_maxkey[mb] = r.key;
   }
-#ifdef GG_TRACE
-  const long long fb_t2 = clock64();
-#endif
-  if (!bmean) store_rows();
-#ifdef GG_TRACE
-  if (lane == 0 && g_trace != nullptr) {
-    const size_t b = static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV;
-    g_trace[b + 24] = fb_t0;
-    g_trace[b + 25] = fb_t1;
-    g_trace[b + 26] = fb_t2;
-    g_trace[b + 27] = clock64();
-  }
-#endif
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  int nf = static_cast<int>(__shfl_sync(0xffffffffu, fin_rows, 0));
-  const unsigned long long mk = __shfl_sync(0xffffffffu, fin_key, 0);
-  if (bmean) {
+}
+
+// The launch summary from the totals (and the batch-mean flags, which need every d).
+template <bool INT>
+__device__ void publish_summary(const Params& p, int lane, int nf, unsigned long long mk) {
+  if (!INT && p.statistic == GG_BATCH_MEAN) {
     double s = 0.0;  // fixed lane -> row assignment and shuffle tree: deterministic
     for (int r = lane; r < p.M; r += 32) s += ldcg_f64(&static_cast<double*>(p.d)[r]);
 #pragma unroll
@@ -206,6 +177,62 @@ __device__ void finish_band(const Params& p, int mb, int lane, const double (&ob
     *p.triggered = nf > 0 ? 1 : 0;
     *p.max_disc = (mk == 0ull) ? __longlong_as_double(0x7FF0000000000000ll)
                                : __longlong_as_double(static_cast<long long>(mk - 1ull));
+  }
+}
+
+// d / flags of band mb, its band summary and, for the band that completes the launch's
+// count, the launch summaries (nflag, triggered, max_disc).  One warp.
+template <bool INT>
+__device__ void finish_band(const Params& p, int mb, int lane, const double (&obs_f)[4], const double (&pred_f)[4],
+                            const long long (&obs_i)[4], const long long (&pred_i)[4]) {
+#ifdef GG_TRACE
+  const long long fb_t0 = clock64();
+#endif
+  const bool bmean = !INT && p.statistic == GG_BATCH_MEAN;
+  const BandRows<INT> r = band_rows<INT>(p, mb, lane, obs_f, pred_f, obs_i, pred_i);
+#ifdef GG_TRACE
+  const long long fb_t1 = clock64();
+#endif
+  // Launch summary: atomicMax of the band's gap key, then a release-add of
+  // {1 << 32 | flagged rows}; the band that completes the count acquires and reads the
+  // totals.  The release has no outstanding stores to wait for when the rows are stored
+  // after it (the batch-mean statistic reads every row's d, so there they go first).
+  if (bmean) {
+    store_band<INT>(p, mb, lane, r);
+    __syncwarp();
+  }
+  int last = 0;
+  unsigned long long fin_rows = 0, fin_key = 0;
+  if (lane == 0) {
+    const int total = p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles;
+    atomicMax(&p.ws.summary[1], r.key);
+    const unsigned long long inc = (1ull << 32) | static_cast<unsigned>(r.nflag);
+    const unsigned long long old = atom_add_release_gpu_u64(&p.ws.summary[0], inc);
+    last = (static_cast<long long>(old >> 32) + 1 == total) ? 1 : 0;
+    if (last) {
+      fence_acquire_gpu();
+      fin_rows = (old + inc) & 0xFFFFFFFFull;
+      fin_key = atomicMax(&p.ws.summary[1], 0ull);
+    }
+  }
+#ifdef GG_TRACE
+  const long long fb_t2 = clock64();
+#endif
+  if (!bmean) store_band<INT>(p, mb, lane, r);
+#ifdef GG_TRACE
+  if (lane == 0 && g_trace != nullptr) {
+    const size_t b = static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV;
+    g_trace[b + 24] = fb_t0;
+    g_trace[b + 25] = fb_t1;
+    g_trace[b + 26] = fb_t2;
+    g_trace[b + 27] = clock64();
+  }
+#endif
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  publish_summary<INT>(p, lane, static_cast<int>(__shfl_sync(0xffffffffu, fin_rows, 0)),
+                       __shfl_sync(0xffffffffu, fin_key, 0));
+  if (lane == 0) {
     p.ws.summary[0] = 0ull;  // every band has counted: the workspace is left ready
     p.ws.summary[1] = 0ull;
   }
@@ -576,6 +603,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         finish_band<INT>(p, mb, lane, of, pf, oi, pi);
       };
+      // ascending-tile fold of band b's workspace partials; the loads of four tiles are in flight together
+      auto fold_band = [&](int b, unsigned long long (&bo)[4], unsigned long long (&bpr)[4]) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { bo[q] = 0ull; bpr[q] = 0ull; }
+        for (int tt0 = 0; tt0 < n_tiles; tt0 += 4) {
+          unsigned long long vo[4][4], vp[4][4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              vo[j][q] = 0ull;
+              vp[j][q] = 0ull;
+              if (tt0 + j < n_tiles) {
+                const size_t g = static_cast<size_t>(tt0 + j) * p.m_pad + b * BM + lane + 32 * q;
+                vo[j][q] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpart + g)));
+                vp[j][q] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpred + g)));
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (tt0 + j >= n_tiles) break;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              bo[q] = acc_add<OBS_MODE>(bo[q], vo[j][q]);
+              bpr[q] = acc_add<PRED_MODE>(bpr[q], vp[j][q]);
+            }
+          }
+        }
+      };
       unsigned long long ao[4] = {0ull, 0ull, 0ull, 0ull}, ap[4] = {0ull, 0ull, 0ull, 0ull};
       int local = 0;
       for (int i_seq = 0; i_seq < n_seq; ++i_seq) {
@@ -591,7 +648,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lane == 0) GG_EV(8, local);
         const int mb = 2 * m + static_cast<int>(rank);
         const bool band_ok = mb < p.m_tiles && (!p.replay || p.ws.band_active[mb]) && !(p.dbg & 4);
-        const bool whole = !p.sched && (m * n_tiles >= t0) && ((m + 1) * n_tiles <= t1);  // band folded locally
+        // band folded locally (tiny launches fold every band in one place, below)
+        const bool whole = !p.sched && !p.tiny && (m * n_tiles >= t0) && ((m + 1) * n_tiles <= t1);
         if (band_ok) {
           if (whole && n == 0) {
 #pragma unroll
@@ -623,49 +681,81 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (band_ok) {
           if (whole) {
             if (n == n_tiles - 1 && !(p.dbg & 64)) finish(mb, ao, ap);
-          } else if ((p.sched || t == min((m + 1) * n_tiles, t1) - 1) && !(p.dbg & 128)) {
+          } else if ((p.sched || p.tiny || t == min((m + 1) * n_tiles, t1) - 1) && !(p.dbg & 128)) {
             // the pair's last tile of this band: release its partials with one count of the
-            // tiles it contributed (contiguous schedule: at most two such parts per pair)
-            const int part = p.sched ? 1 : min((m + 1) * n_tiles, t1) - max(m * n_tiles, t0);
+            // tiles it contributed (contiguous schedule: at most two such parts per pair).
+            // Tiny launches (at most one tile per pair) count on one launch-wide counter and
+            // the last tile of the launch folds every band and publishes the summary itself.
+            const int part = (p.sched || p.tiny) ? 1 : min((m + 1) * n_tiles, t1) - max(m * n_tiles, t0);
+            int* counter = p.tiny ? &p.ws.counters[3] : &p.ws.band_counter[mb];
             __syncwarp();
             int last = 0;
             if (lane == 0) {
-              last = (atom_add_release_gpu(&p.ws.band_counter[mb], part) == n_tiles - part) ? 1 : 0;
+              const int total = p.tiny ? n_tiles * (p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles) : n_tiles;
+              last = (atom_add_release_gpu(counter, part) == total - part) ? 1 : 0;
               if (last) {
                 fence_acquire_gpu();  // the other pairs' partials
-                p.ws.band_counter[mb] = 0;
+                *counter = 0;
               }
             }
             last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) {
-              unsigned long long bo[4] = {0ull, 0ull, 0ull, 0ull}, bpr[4] = {0ull, 0ull, 0ull, 0ull};
-              // ascending-tile fold; the loads of four tiles are in flight together
-              for (int tt0 = 0; tt0 < n_tiles; tt0 += 4) {
-                unsigned long long vo[4][4], vp[4][4];
+            if (last && !p.tiny) {
+              unsigned long long bo[4], bpr[4];
+              fold_band(mb, bo, bpr);
+              finish(mb, bo, bpr);
+            } else if (last) {
+              // every band's partials in one burst of async copies into this CTA's (now idle)
+              // pipeline stages: [band][tile][obs, pred][128 rows] (m_tiles * n_tiles <= 64)
+              const uint32_t sbuf = smem_u32(smA);
+              for (int b = 0; b < p.m_tiles; ++b) {
+                if (p.replay && !p.ws.band_active[b]) continue;
+                for (int tt = 0; tt < n_tiles; ++tt) {
+                  const size_t g = static_cast<size_t>(tt) * p.m_pad + b * BM + 2 * lane;
+                  const uint32_t d0 = sbuf + static_cast<uint32_t>(((b * n_tiles + tt) * 2) * BM * 8 + lane * 16);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    vo[j][q] = 0ull;
-                    vp[j][q] = 0ull;
-                    if (tt0 + j < n_tiles) {
-                      const size_t g = static_cast<size_t>(tt0 + j) * p.m_pad + mb * BM + lane + 32 * q;
-                      vo[j][q] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpart + g)));
-                      vp[j][q] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpred + g)));
-                    }
-                  }
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  if (tt0 + j >= n_tiles) break;
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    bo[q] = acc_add<OBS_MODE>(bo[q], vo[j][q]);
-                    bpr[q] = acc_add<PRED_MODE>(bpr[q], vp[j][q]);
+                  for (int h = 0; h < 2; ++h) {  // rows 2*lane + 64h .. +1
+                    cp_async16(d0 + h * 512, gpart + g + 64 * h);
+                    cp_async16(d0 + BM * 8 + h * 512, gpred + g + 64 * h);
                   }
                 }
               }
-              finish(mb, bo, bpr);
+              cp_async_wait_all();
+              __syncwarp();
+              const unsigned long long* sv = reinterpret_cast<const unsigned long long*>(smA);
+              int nf = 0;
+              unsigned long long mk = 0;
+              for (int b = 0; b < p.m_tiles; ++b) {
+                if (p.replay && !p.ws.band_active[b]) {
+                  nf += __ldcg(&p.ws.band_nflag[b]);  // standing summary of an untouched band
+                  const unsigned long long k = __ldcg(&p.ws.band_maxkey[b]);
+                  mk = k > mk ? k : mk;
+                  continue;
+                }
+                unsigned long long bo[4] = {0ull, 0ull, 0ull, 0ull}, bpr[4] = {0ull, 0ull, 0ull, 0ull};
+                for (int tt = 0; tt < n_tiles; ++tt) {  // ascending tiles, as fold_band
+                  const unsigned long long* base = sv + static_cast<size_t>((b * n_tiles + tt) * 2) * BM;
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    bo[q] = acc_add<OBS_MODE>(bo[q], base[lane + 32 * q]);
+                    bpr[q] = acc_add<PRED_MODE>(bpr[q], base[BM + lane + 32 * q]);
+                  }
+                }
+                double of[4], pf[4];
+                long long oi[4], pi[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  oi[q] = static_cast<long long>(bo[q]);
+                  pi[q] = static_cast<long long>(bpr[q]);
+                  of[q] = INT ? 0.0 : acc_f64<OBS_MODE>(bo[q]);
+                  pf[q] = INT ? 0.0 : acc_f64<PRED_MODE>(bpr[q]);
+                }
+                const BandRows<INT> r = band_rows<INT>(p, b, lane, of, pf, oi, pi);
+                store_band<INT>(p, b, lane, r);
+                nf += r.nflag;
+                mk = r.key > mk ? r.key : mk;
+              }
+              __syncwarp();
+              publish_summary<INT>(p, lane, nf, mk);
             }
           }
         }

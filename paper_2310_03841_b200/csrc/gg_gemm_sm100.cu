@@ -329,6 +329,8 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   if (p.dbg & 1024) p.sched = 0;  // diagnostics: force a schedule
   if (p.dbg & 2048) p.sched = 1;
   if (replay) p.sched = 1;  // replay walks the listed band pairs strided; every band folds via the workspace
+  // tiny launches (at most one tile per pair, few bands): one launch-wide fold from smem
+  p.tiny = (pair_tiles <= pairs && p.m_tiles <= 4 && p.m_tiles * p.n_tiles <= 64) ? 1 : 0;
 
   switch (kind) {
     case K_BF16:

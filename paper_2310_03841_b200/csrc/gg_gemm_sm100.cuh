@@ -24,7 +24,7 @@ enum : int { O_BF16 = 0, O_F16 = 1, O_F32 = 2, O_I32 = 3 };
 
 struct Workspace {
   unsigned long long* summary;  // [2] {done bands << 32 | flagged rows, max gap key}: one 128-bit CAS per band
-  int* counters;        // [1] active 128-row bands, [2] active 256-row band pairs (replay)
+  int* counters;        // [1] active 128-row bands, [2] active 256-row band pairs (replay), [3] tiny-launch tiles
   int* active_pairs;    // [m_pairs] replay: ascending list of the band pairs to recompute
   int* band_counter;    // [m_tiles]
   uint8_t* band_active; // [m_tiles]
@@ -59,6 +59,7 @@ struct Params {
   int n_inj;
   int c_tma;            // 1: C is stored through smem boxes + TMA (needs 16 B aligned C and pitch)
   int sched;            // 0: contiguous tile range per pair, 1: strided (long K)
+  int tiny;             // <= 1 tile per pair, <= 4 bands: one launch-wide fold from smem (fewest round trips)
   int dbg;              // diagnostics only ($GG_DEBUG), 0 in production: 1 skip predicted dot products,
                         // 2 decouple the checksum warps from the stages, 4 skip band folds, 8 skip
                         // observed sums, 64 skip local band finishes, 128 skip split-band exchanges,
