@@ -106,9 +106,13 @@ _WS: dict[tuple, torch.Tensor] = {}
 
 
 def workspace(M: int, N: int, device: torch.device, key=None) -> torch.Tensor:
-    """Zero-initialised workspace for (M, N); every launch leaves it re-zeroed."""
+    """Zero-initialised workspace for (M, N); every launch leaves it re-zeroed.
+
+    One workspace per (device, shape, key, stream): launches on one stream are
+    ordered, so they may share it (a replay finds its launch's band summaries),
+    while launches on different streams never race on the same counters."""
     nbytes = int(L.load().gg_protected_gemm_workspace_bytes(M, N))
-    k = (device, M, N, key)
+    k = (device, M, N, key, torch.cuda.current_stream(device).cuda_stream)
     ws = _WS.get(k)
     if ws is None or ws.numel() < nbytes:
         ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)

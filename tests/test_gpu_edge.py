@@ -127,3 +127,26 @@ def test_replay_under_strided_schedule_at_scale(dtype):
     assert int(changed.item()) == 3
     assert torch.equal(y.view(torch.uint8), clean.view(torch.uint8))
     assert int(res.nflag.item()) == 0
+
+
+def test_concurrent_streams_same_shape_do_not_share_counters():
+    M, N, Kd = 4096, 768, 768
+    x, w, b, ws, bs = _ops(M, N, Kd, torch.bfloat16, 21)
+    x2 = torch.randn(M, Kd, device="cuda").to(torch.bfloat16)
+    ref1, r1 = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
+    ref2, r2 = K.protected_gemm(x2, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
+    torch.cuda.synchronize()
+    d1, d2 = r1.d.clone(), r2.d.clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(20):
+        with torch.cuda.stream(s1):
+            ya, ra = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
+        with torch.cuda.stream(s2):
+            yb, rb = K.protected_gemm(x2, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
+        outs.append((ya, ra, yb, rb))
+    torch.cuda.synchronize()
+    for ya, ra, yb, rb in outs:
+        assert torch.equal(ya, ref1) and torch.equal(yb, ref2)
+        assert torch.equal(ra.d, d1) and torch.equal(rb.d, d2)
+        assert int(ra.nflag.item()) == 0 and int(rb.nflag.item()) == 0
