@@ -110,7 +110,7 @@ def build_variant(name: str, defines: list[str]) -> Path:
 
 def build_trace(verbose: bool = False) -> Path:
     """-DGG_TRACE: per-tile clock64 stamps of every warp role (tools/trace_tiles.py)."""
-    return build_variant("trace", ["-DGG_TRACE"])
+    return build_variant("trace", ["-DGG_TRACE", "-DGG_DIAGNOSTICS"])
 
 
 if __name__ == "__main__":

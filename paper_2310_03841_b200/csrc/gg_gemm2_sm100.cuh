@@ -61,6 +61,14 @@ constexpr int TRACE_TILES = 64, TRACE_EV = 28;
   } while (0)
 #endif
 
+// Diagnostic switches ($GG_DEBUG, Params::dbg) exist only in diagnostics builds
+// (python -m paper_2310_03841_b200.build --trace / --variant diag GG_DIAGNOSTICS).
+#ifdef GG_DIAGNOSTICS
+#define GG_DBG(bit) ((p.dbg & (bit)) != 0)
+#else
+#define GG_DBG(bit) false
+#endif
+
 constexpr int BM = 128;           // rows per CTA (256 per pair)
 constexpr int BN = 256;           // MMA N per tile; each CTA stages BN/2 rows of B
 constexpr int BK_BYTES = 128;     // one 128 B swizzle atom of K per stage
@@ -501,7 +509,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const long long tw1 = clock64();
           tr_empty += tw1 - tw0;
 #endif
-          if ((chk_pending & (1u << stage)) && !(p.dbg & 2)) {  // the checksum warps still hold the stage's previous K-block
+          if ((chk_pending & (1u << stage)) && !GG_DBG(2)) {  // the checksum warps still hold the stage's previous K-block
             mbar_wait(&chkdone_bar[stage], (chk_phase >> stage) & 1u);
 #ifdef GG_TRACE
             tr_chk += clock64() - tw1;
@@ -557,7 +565,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #ifdef GG_TRACE
           tr_full += clock64() - tf0;
 #endif
-          if (mine && !(p.dbg & 2)) {  // both CTAs' halves of this stage have landed: let the checksum warps copy A
+          if (mine && !GG_DBG(2)) {  // both CTAs' halves of this stage have landed: let the checksum warps copy A
             mbar_arrive(&aready_bar[stage]);
             mbar_arrive_cluster(aready_peer + static_cast<uint32_t>(stage * 8));
           }
@@ -647,7 +655,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         mbar_wait(&pfull_bar[slot], ph);
         if (lane == 0) GG_EV(8, local);
         const int mb = 2 * m + static_cast<int>(rank);
-        const bool band_ok = mb < p.m_tiles && (!p.replay || p.ws.band_active[mb]) && !(p.dbg & 4);
+        const bool band_ok = mb < p.m_tiles && (!p.replay || p.ws.band_active[mb]) && !GG_DBG(4);
         // band folded locally (tiny launches fold every band in one place, below)
         const bool whole = !p.sched && !p.tiny && (m * n_tiles >= t0) && ((m + 1) * n_tiles <= t1);
         if (band_ok) {
@@ -680,8 +688,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         if (band_ok) {
           if (whole) {
-            if (n == n_tiles - 1 && !(p.dbg & 64)) finish(mb, ao, ap);
-          } else if ((p.sched || p.tiny || t == min((m + 1) * n_tiles, t1) - 1) && !(p.dbg & 128)) {
+            if (n == n_tiles - 1 && !GG_DBG(64)) finish(mb, ao, ap);
+          } else if ((p.sched || p.tiny || t == min((m + 1) * n_tiles, t1) - 1) && !GG_DBG(128)) {
             // the pair's last tile of this band: release its partials with one count of the
             // tiles it contributed (contiguous schedule: at most two such parts per pair).
             // Tiny launches (at most one tile per pair) count on one launch-wide counter and
@@ -914,7 +922,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         GG_LAP(tr_cmp);
         if constexpr (PROTECT) {  // observed row sum of the STORED values (guard.py:170)
-          if (row_ok && !(p.dbg & 8)) {
+          if (row_ok && !GG_DBG(8)) {
             if constexpr (INT) {
               if (full) {
                 // exact: v = hi16 * 2^16 + lo16 (lo unsigned, hi signed); each half summed by one
@@ -1086,7 +1094,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #ifdef GG_TRACE
         const long long c0 = clock64();
 #endif
-        if (p.dbg & 2) {
+        if (GG_DBG(2)) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) v[j] = make_uint4(kb, s, tid, 0);
           return;
@@ -1133,7 +1141,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #ifdef GG_TRACE
           const long long cp0 = clock64();
 #endif
-          if (p.dbg & 1) { hi += vc[0].x; accd += vc[0].x; acci += vc[1].y; continue; }
+          if (GG_DBG(1)) { hi += vc[0].x; accd += vc[0].x; acci += vc[1].y; continue; }
           // w-vectors are zero-padded to whole K-blocks (gg_checksum_aux) and TMA zero-fills
           // x beyond K: no tail checks.  Independent accumulators for ILP.
           if (w_smem) chk_dot<KIND, true>(v, kb, w_sm_addr, p.w_aux, hi, lo, accd, acci);

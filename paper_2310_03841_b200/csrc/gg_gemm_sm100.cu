@@ -326,8 +326,10 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   // A bands streamed concurrently by all pairs (256 rows x K each): keep them L2-resident
   const double a_footprint = static_cast<double>(pairs) * 2 * pair::BM * static_cast<double>(d->K) * elem;
   p.sched = a_footprint > 40.0e6 ? 1 : 0;
+#ifdef GG_DIAGNOSTICS
   if (p.dbg & 1024) p.sched = 0;  // diagnostics: force a schedule
   if (p.dbg & 2048) p.sched = 1;
+#endif
   if (replay) p.sched = 1;  // replay walks the listed band pairs strided; every band folds via the workspace
   // tiny launches (at most one tile per pair, few bands): one launch-wide fold from smem
   p.tiny = (pair_tiles <= pairs && p.m_tiles <= 4 && p.m_tiles * p.n_tiles <= 64) ? 1 : 0;
