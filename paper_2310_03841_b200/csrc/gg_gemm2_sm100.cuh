@@ -471,6 +471,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync_all();  // barrier inits and the TMEM allocation visible to both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the setup above overlapped the previous kernel's tail;
+  // nothing below may read memory before that kernel has completed.  The next launch may
+  // be scheduled as our CTAs retire.
+#ifndef GG_NO_PDL
+  pdl_wait();
+  pdl_launch_dependents();
+#endif
 
   // replay: a pair tile is recomputed when either of its two 128-row bands is active
   auto pair_active = [&](int m) -> bool {

@@ -175,7 +175,23 @@ int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
       return fail(GG_ECUDA, "cudaFuncSetAttribute(max dynamic smem, pair kernel) failed");
     configured = true;
   }
+#ifdef GG_NO_PDL
   kern<<<grid, pair::THREADS, pair::SMEM_BYTES, s>>>(ta, tb, tc, p);
+#else
+  // programmatic dependent launch: the CTA setup overlaps the previous kernel's tail (the
+  // kernel waits on griddepcontrol before touching memory)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(pair::THREADS);
+  cfg.dynamicSmemBytes = pair::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p);
+#endif
   return check_launch("protected_gemm_pair");
 }
 

@@ -34,6 +34,12 @@ __device__ __forceinline__ unsigned long long atom_add_release_gpu_u64(unsigned 
   asm volatile("atom.release.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(addr), "l"(v) : "memory");
   return old;
 }
+// Programmatic dependent launch: let the next grid on the stream be scheduled early /
+// wait until the previous grid has completed and its memory is visible (no-ops when the
+// launch carried no programmatic dependency).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 16-byte global -> shared asynchronous copy (L2 only) and its completion wait.
 __device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gsrc) : "memory");
