@@ -385,6 +385,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   constexpr int MMAS_PER_STAGE = BK_BYTES / MMA_K_BYTES;
   constexpr bool OUT16 = (OUT == O_BF16 || OUT == O_F16);
   constexpr bool PRED_PAIR = (KIND == K_BF16 || KIND == K_F16);  // predicted partials as fp32 (hi, lo)
+  constexpr int OBS_MODE = INT ? ACC_I64 : (OUT16 ? ACC_DF : ACC_F64);
+  constexpr int PRED_MODE = INT ? ACC_I64 : (PRED_PAIR ? ACC_DF : ACC_F64);
   constexpr uint32_t IDESC = PairIdesc<KIND>::V;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -436,6 +438,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     i -= hb - t0;
     if (i < t1 - tb) return tb + i;
     return hb + (i - (t1 - tb));
+  };
+
+  // A band pair is folded where it is computed when one pair computes all its N-tiles in
+  // order (contiguous schedule, not cut by a range boundary, not a tiny launch): its
+  // epilogue and checksum warps keep band totals and hand over once, at the band's last
+  // tile.  Other bands hand over every tile and fold through the workspace.  Both paths
+  // fold in the same association: per column half, ascending tiles, then the halves.
+  auto band_whole = [&](int m) -> bool {
+    return !p.sched && !p.tiny && (m * n_tiles >= t0) && ((m + 1) * n_tiles <= t1);
   };
 
   // warp roles; the SMSP arbiter issues highest-warp-id first, so the ids follow criticality
@@ -599,8 +610,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else if (warp == W_REDUCER) {
     // ================================================= reducer
     if constexpr (PROTECT) {
-      constexpr int OBS_MODE = INT ? ACC_I64 : (OUT16 ? ACC_DF : ACC_F64);
-      constexpr int PRED_MODE = INT ? ACC_I64 : (PRED_PAIR ? ACC_DF : ACC_F64);
       const unsigned long long* so = reinterpret_cast<const unsigned long long*>(slot_obs);
       const unsigned long long* sp = reinterpret_cast<const unsigned long long*>(slot_pred);
       unsigned long long* gpart = reinterpret_cast<unsigned long long*>(p.ws.partial);
@@ -618,21 +627,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         finish_band<INT>(p, mb, lane, of, pf, oi, pi);
       };
-      // ascending-tile fold of band b's workspace partials; the loads of four tiles are in flight together
+      // workspace partials of split bands: observed per column half ([half][tile][row]) and predicted
+      const size_t half_stride = static_cast<size_t>(n_tiles) * p.m_pad;
+      // ascending-tile fold of band b's workspace partials: per half, then the halves (the same
+      // association as a band folded where it was computed); four tiles' loads in flight together
       auto fold_band = [&](int b, unsigned long long (&bo)[4], unsigned long long (&bpr)[4]) {
+        unsigned long long b0[4], b1[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) { bo[q] = 0ull; bpr[q] = 0ull; }
+        for (int q = 0; q < 4; ++q) { b0[q] = 0ull; b1[q] = 0ull; bpr[q] = 0ull; }
         for (int tt0 = 0; tt0 < n_tiles; tt0 += 4) {
-          unsigned long long vo[4][4], vp[4][4];
+          unsigned long long v0[4][4], v1[4][4], vp[4][4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              vo[j][q] = 0ull;
-              vp[j][q] = 0ull;
+              v0[j][q] = v1[j][q] = vp[j][q] = 0ull;
               if (tt0 + j < n_tiles) {
                 const size_t g = static_cast<size_t>(tt0 + j) * p.m_pad + b * BM + lane + 32 * q;
-                vo[j][q] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpart + g)));
+                v0[j][q] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpart + g)));
+                v1[j][q] = static_cast<unsigned long long>(
+                    ldcg_i64(reinterpret_cast<const long long*>(gpart + half_stride + g)));
                 vp[j][q] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpred + g)));
               }
             }
@@ -642,20 +656,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if (tt0 + j >= n_tiles) break;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              bo[q] = acc_add<OBS_MODE>(bo[q], vo[j][q]);
+              b0[q] = acc_add<OBS_MODE>(b0[q], v0[j][q]);
+              b1[q] = acc_add<OBS_MODE>(b1[q], v1[j][q]);
               bpr[q] = acc_add<PRED_MODE>(bpr[q], vp[j][q]);
             }
           }
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bo[q] = acc_add<OBS_MODE>(b0[q], b1[q]);
       };
-      unsigned long long ao[4] = {0ull, 0ull, 0ull, 0ull}, ap[4] = {0ull, 0ull, 0ull, 0ull};
-      int local = 0;
+      int local = 0, sloti = 0;
       for (int i_seq = 0; i_seq < n_seq; ++i_seq) {
         const int t = tile_at(i_seq);
         const int m = t / n_tiles, n = t - m * n_tiles;
         if (!pair_active(m)) continue;
-        const int slot = local % NSLOT;
-        const uint32_t ph = static_cast<uint32_t>(local / NSLOT) & 1u;
+        // band folded where it was computed: one hand-over, at the band's last tile
+        const bool whole = band_whole(m);
+        if (whole && n != n_tiles - 1) {
+          ++local;
+          continue;
+        }
+        const int slot = sloti % NSLOT;
+        const uint32_t ph = static_cast<uint32_t>(sloti / NSLOT) & 1u;
+        ++sloti;
         if (lane == 0) GG_EV(11, local);
         mbar_wait(&ofull_bar[slot], ph);
         if (lane == 0) GG_EV(12, local);
@@ -663,28 +686,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lane == 0) GG_EV(8, local);
         const int mb = 2 * m + static_cast<int>(rank);
         const bool band_ok = mb < p.m_tiles && (!p.replay || p.ws.band_active[mb]) && !GG_DBG(4);
-        // band folded locally (tiny launches fold every band in one place, below)
-        const bool whole = !p.sched && !p.tiny && (m * n_tiles >= t0) && ((m + 1) * n_tiles <= t1);
+        unsigned long long ao[4], ap[4];
         if (band_ok) {
-          if (whole && n == 0) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) { ao[q] = 0ull; ap[q] = 0ull; }
-          }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int i = lane + 32 * q;
             const int io = 2 * slot * BM + i;  // half 0, then half 1 (+BM)
-            // this tile's observed partial (both column halves) and predicted partial; the
-            // ascending-tile fold below is the same for local and split bands
-            const unsigned long long to = acc_add<OBS_MODE>(so[io], so[io + BM]);
-            const unsigned long long tp = sp[slot * BM + i];
-            if (whole) {
-              ao[q] = acc_add<OBS_MODE>(ao[q], to);
-              ap[q] = acc_add<PRED_MODE>(ap[q], tp);
-            } else {
+            const unsigned long long h0 = so[io], h1 = so[io + BM], pv = sp[slot * BM + i];
+            if (whole) {  // band totals per half: combine the halves
+              ao[q] = acc_add<OBS_MODE>(h0, h1);
+              ap[q] = pv;
+            } else {      // this tile's partials, per half, into the workspace
               const size_t g = static_cast<size_t>(n) * p.m_pad + mb * BM + i;
-              gpart[g] = to;
-              gpred[g] = tp;
+              gpart[g] = h0;
+              gpart[half_stride + g] = h1;
+              gpred[g] = pv;
             }
           }
         }
@@ -695,7 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         if (band_ok) {
           if (whole) {
-            if (n == n_tiles - 1 && !GG_DBG(64)) finish(mb, ao, ap);
+            if (!GG_DBG(64)) finish(mb, ao, ap);
           } else if ((p.sched || p.tiny || t == min((m + 1) * n_tiles, t1) - 1) && !GG_DBG(128)) {
             // the pair's last tile of this band: release its partials with one count of the
             // tiles it contributed (contiguous schedule: at most two such parts per pair).
@@ -720,17 +736,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               finish(mb, bo, bpr);
             } else if (last) {
               // every band's partials in one burst of async copies into this CTA's (now idle)
-              // pipeline stages: [band][tile][obs, pred][128 rows] (m_tiles * n_tiles <= 64)
+              // pipeline stages: [band][tile][obs half 0, obs half 1, pred][128 rows]
+              // (m_tiles * n_tiles <= 48)
               const uint32_t sbuf = smem_u32(smA);
               for (int b = 0; b < p.m_tiles; ++b) {
                 if (p.replay && !p.ws.band_active[b]) continue;
                 for (int tt = 0; tt < n_tiles; ++tt) {
                   const size_t g = static_cast<size_t>(tt) * p.m_pad + b * BM + 2 * lane;
-                  const uint32_t d0 = sbuf + static_cast<uint32_t>(((b * n_tiles + tt) * 2) * BM * 8 + lane * 16);
+                  const uint32_t d0 = sbuf + static_cast<uint32_t>(((b * n_tiles + tt) * 3) * BM * 8 + lane * 16);
 #pragma unroll
                   for (int h = 0; h < 2; ++h) {  // rows 2*lane + 64h .. +1
                     cp_async16(d0 + h * 512, gpart + g + 64 * h);
-                    cp_async16(d0 + BM * 8 + h * 512, gpred + g + 64 * h);
+                    cp_async16(d0 + BM * 8 + h * 512, gpart + half_stride + g + 64 * h);
+                    cp_async16(d0 + 2 * BM * 8 + h * 512, gpred + g + 64 * h);
                   }
                 }
               }
@@ -746,15 +764,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                   mk = k > mk ? k : mk;
                   continue;
                 }
-                unsigned long long bo[4] = {0ull, 0ull, 0ull, 0ull}, bpr[4] = {0ull, 0ull, 0ull, 0ull};
-                for (int tt = 0; tt < n_tiles; ++tt) {  // ascending tiles, as fold_band
-                  const unsigned long long* base = sv + static_cast<size_t>((b * n_tiles + tt) * 2) * BM;
+                unsigned long long bo[4], bpr[4], b0[4] = {0ull, 0ull, 0ull, 0ull}, b1[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) bpr[q] = 0ull;
+                for (int tt = 0; tt < n_tiles; ++tt) {  // ascending tiles per half, as fold_band
+                  const unsigned long long* base = sv + static_cast<size_t>((b * n_tiles + tt) * 3) * BM;
 #pragma unroll
                   for (int q = 0; q < 4; ++q) {
-                    bo[q] = acc_add<OBS_MODE>(bo[q], base[lane + 32 * q]);
-                    bpr[q] = acc_add<PRED_MODE>(bpr[q], base[BM + lane + 32 * q]);
+                    b0[q] = acc_add<OBS_MODE>(b0[q], base[lane + 32 * q]);
+                    b1[q] = acc_add<OBS_MODE>(b1[q], base[BM + lane + 32 * q]);
+                    bpr[q] = acc_add<PRED_MODE>(bpr[q], base[2 * BM + lane + 32 * q]);
                   }
                 }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) bo[q] = acc_add<OBS_MODE>(b0[q], b1[q]);
                 double of[4], pf[4];
                 long long oi[4], pi[4];
 #pragma unroll
@@ -790,6 +813,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     int cbuf = 0;
     int local = 0;
+    int sloti = 0;                       // hand-overs so far (the reducer's slot sequence)
+    unsigned long long band_obs = 0ull;  // whole bands: running total over the band's tiles
     // bias of a tile's 256 columns, one value per epilogue thread, loaded one tile ahead (its
     // latency is off the critical path) and staged in shared memory for the broadcast reads below
     const uint32_t* bias_g = static_cast<const uint32_t*>(p.bias);
@@ -1056,17 +1081,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
 #endif
       if constexpr (PROTECT) {
-        const int slot = local % NSLOT;
-        mbar_wait(&oempty_bar[slot], (static_cast<uint32_t>(local / NSLOT) & 1u) ^ 1u);
-        if (lead) GG_EV(3, local);
-        const int io = (2 * slot + half) * BM + tid;
+        unsigned long long tile_obs;  // this (row, column half)'s partial of the tile, OBS_MODE bits
         if constexpr (INT)
-          reinterpret_cast<long long*>(slot_obs)[io] =
-              obs_i + static_cast<long long>(obs_ihi) * 65536ll + static_cast<long long>(obs_ilo);
-        else if constexpr (OUT16) reinterpret_cast<float2*>(slot_obs)[io] = make_float2(obs_hi, obs_lo);
-        else slot_obs[io] = obs;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ofull_bar[slot]);
+          tile_obs = static_cast<unsigned long long>(obs_i + static_cast<long long>(obs_ihi) * 65536ll +
+                                                     static_cast<long long>(obs_ilo));
+        else if constexpr (OUT16)
+          tile_obs = static_cast<unsigned long long>(__float_as_uint(obs_hi)) |
+                     (static_cast<unsigned long long>(__float_as_uint(obs_lo)) << 32);
+        else
+          tile_obs = static_cast<unsigned long long>(__double_as_longlong(obs));
+        const bool whole = band_whole(m);
+        if (whole) band_obs = acc_add<OBS_MODE>(n == 0 ? 0ull : band_obs, tile_obs);
+        if (!whole || n == n_tiles - 1) {  // hand over: the tile's partial, or the band's total
+          const int slot = sloti % NSLOT;
+          mbar_wait(&oempty_bar[slot], (static_cast<uint32_t>(sloti / NSLOT) & 1u) ^ 1u);
+          if (lead) GG_EV(3, local);
+          reinterpret_cast<unsigned long long*>(slot_obs)[(2 * slot + half) * BM + tid] = whole ? band_obs : tile_obs;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ofull_bar[slot]);
+          ++sloti;
+        }
       }
       ++local;
     }
@@ -1129,6 +1163,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #endif
       };
       int local = 0;
+      int sloti = 0;                        // hand-overs so far (the reducer's slot sequence)
+      unsigned long long band_pred = 0ull;  // whole bands: running total over the band's tiles
       for (int i_seq = 0; i_seq < n_seq; ++i_seq) {
         const int t = tile_at(i_seq);
         const int m = t / n_tiles, n = t - m * n_tiles;
@@ -1171,15 +1207,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         tc_wait = tc_copy = tc_fence = tc_comp = 0;
 #endif
-        const int slot = local % NSLOT;
-        mbar_wait(&pempty_bar[slot], (static_cast<uint32_t>(local / NSLOT) & 1u) ^ 1u);
-        if (ctid == 0) GG_EV(7, local);
-        if constexpr (INT) reinterpret_cast<long long*>(slot_pred)[slot * BM + tid] = acci;
-        else if constexpr (KIND == K_BF16 || KIND == K_F16)
-          reinterpret_cast<float2*>(slot_pred)[slot * BM + tid] = make_float2(hi, lo);
-        else slot_pred[slot * BM + tid] = accd;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pfull_bar[slot]);
+        unsigned long long tile_pred;  // this row's predicted partial of the tile, PRED_MODE bits
+        if constexpr (INT) tile_pred = static_cast<unsigned long long>(acci);
+        else if constexpr (PRED_PAIR)
+          tile_pred = static_cast<unsigned long long>(__float_as_uint(hi)) |
+                      (static_cast<unsigned long long>(__float_as_uint(lo)) << 32);
+        else tile_pred = static_cast<unsigned long long>(__double_as_longlong(accd));
+        const bool whole = band_whole(m);
+        if (whole) band_pred = acc_add<PRED_MODE>(n == 0 ? 0ull : band_pred, tile_pred);
+        if (!whole || n == n_tiles - 1) {  // hand over: the tile's partial, or the band's total
+          const int slot = sloti % NSLOT;
+          mbar_wait(&pempty_bar[slot], (static_cast<uint32_t>(sloti / NSLOT) & 1u) ^ 1u);
+          if (ctid == 0) GG_EV(7, local);
+          reinterpret_cast<unsigned long long*>(slot_pred)[slot * BM + tid] = whole ? band_pred : tile_pred;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&pfull_bar[slot]);
+          ++sloti;
+        }
         ++local;
       }
     }

@@ -91,7 +91,7 @@ WsLayout ws_layout(int64_t M, int64_t N) {
   L.band_nflag = off; off = align_up(off + 4 * m_tiles, 256);
   L.band_maxkey = off; off = align_up(off + 8 * m_tiles, 256);
   L.pred = off; off = align_up(off + 8 * m_pad * n_tiles, 256);
-  L.partial = off; off = align_up(off + 8 * m_pad * n_tiles, 256);
+  L.partial = off; off = align_up(off + 2 * 8 * m_pad * n_tiles, 256);  // per column half
   L.total = off;
   return L;
 }
@@ -348,7 +348,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
 #endif
   if (replay) p.sched = 1;  // replay walks the listed band pairs strided; every band folds via the workspace
   // tiny launches (at most one tile per pair, few bands): one launch-wide fold from smem
-  p.tiny = (pair_tiles <= pairs && p.m_tiles <= 4 && p.m_tiles * p.n_tiles <= 64) ? 1 : 0;
+  p.tiny = (pair_tiles <= pairs && p.m_tiles <= 4 && p.m_tiles * p.n_tiles <= 48) ? 1 : 0;
 
   switch (kind) {
     case K_BF16:
