@@ -109,26 +109,6 @@ __device__ __forceinline__ unsigned long long gap_key(double gap) {
   return static_cast<unsigned long long>(__double_as_longlong(gap)) + 1ull;
 }
 
-// Store 32 outputs of one row chunk (fast path: full chunk, aligned).
-template <int OUT>
-__device__ __forceinline__ void store_chunk_vec(void* cptr, const uint32_t (&o)[32]) {
-  if constexpr (OUT == O_BF16 || OUT == O_F16) {
-    uint4* dst = reinterpret_cast<uint4*>(cptr);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 v;
-      v.x = (o[8 * q + 0] & 0xFFFFu) | (o[8 * q + 1] << 16);
-      v.y = (o[8 * q + 2] & 0xFFFFu) | (o[8 * q + 3] << 16);
-      v.z = (o[8 * q + 4] & 0xFFFFu) | (o[8 * q + 5] << 16);
-      v.w = (o[8 * q + 6] & 0xFFFFu) | (o[8 * q + 7] << 16);
-      dst[q] = v;
-    }
-  } else {
-    uint4* dst = reinterpret_cast<uint4*>(cptr);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-  }
-}
 
 template <int OUT>
 __device__ __forceinline__ uint32_t load_out_bits(const void* base, long long idx) {
