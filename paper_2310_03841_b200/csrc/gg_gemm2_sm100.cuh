@@ -957,12 +957,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (row_ok && !GG_DBG(8)) {
             if constexpr (INT) {
               if (full) {
-                // exact: v = hi16 * 2^16 + lo16 (lo unsigned, hi signed); each half summed by one
-                // IDP2A into int32 sums that cannot overflow over this thread's <= 128 outputs
+                // exact: v = hi16 * 2^16 + lo16 (lo unsigned, hi signed); the halves of two outputs
+                // are gathered by PRMT (ALU pipe) and summed by one IDP2A each, into int32 sums that
+                // cannot overflow over this thread's <= 128 outputs
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                  obs_ilo = __dp2a_lo(o[j], 0x0001u, obs_ilo);                   // + lo16 (unsigned)
-                  obs_ihi = __dp2a_lo(static_cast<int>(o[j]), 0x0100, obs_ihi);  // + hi16 (signed)
+                for (int j = 0; j < 16; ++j) {  // two outputs per IDP2A: their halves gathered by PRMT
+                  const uint32_t lo2 = __byte_perm(o[2 * j], o[2 * j + 1], 0x5410u);
+                  const uint32_t hi2 = __byte_perm(o[2 * j], o[2 * j + 1], 0x7632u);
+                  obs_ilo = __dp2a_lo(lo2, 0x0101u, obs_ilo);                   // + both lo16 (unsigned)
+                  obs_ihi = __dp2a_lo(static_cast<int>(hi2), 0x0101, obs_ihi);  // + both hi16 (signed)
                 }
               } else {
                 long long s = 0;
