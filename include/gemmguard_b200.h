@@ -162,7 +162,7 @@ GG_API int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_
  *   GG_BF16 / GG_F16: float [Kp]  = fp32(w_sum); bf16/fp16 x are exact in fp32,
  *                     so x*w is one fp32 FMA (|w - w_sum| <= 2^-24 |w_sum|),
  *                     folded into fp64 once per K-block of 64;
- *   GG_F32 (tf32):    double [Kp] = w_sum (fp64 products of the fp32 x);
+ *   GG_F32 (tf32):    float  [Kp] = fp32(w_sum) (as the 16-bit kinds);
  *   GG_I8:            int32x4 [Kp/4] signed base-256 digit planes of the int64
  *                     w_sum (|w_sum| < 2^23), so x*w_sum is an exact IDP4A dot. */
 GG_API size_t gg_checksum_aux_bytes(int32_t ab_kind, int64_t K);

@@ -448,11 +448,6 @@ __global__ void f32_of_f64_kernel(const double* w, int64_t K, int64_t Kp, float*
   if (k >= Kp) return;
   out[k] = k < K ? __double2float_rn(w[k]) : 0.f;
 }
-__global__ void f64_copy_kernel(const double* w, int64_t K, int64_t Kp, double* out) {
-  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k >= Kp) return;
-  out[k] = k < K ? w[k] : 0.0;
-}
 __global__ void digits_i64_kernel(const long long* w, int64_t K, int64_t Kp, int4* out) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // group of 4 k
   if (i * 4 >= Kp) return;
@@ -585,8 +580,7 @@ size_t checksum_aux_bytes(int ab_kind, int64_t K) {
   if (K < 1) return 0;
   const int64_t Kp = aux_padded(K);
   switch (ab_kind) {
-    case GG_BF16: case GG_F16: return static_cast<size_t>(Kp) * 4;
-    case GG_F32: return static_cast<size_t>(Kp) * 8;
+    case GG_BF16: case GG_F16: case GG_F32: return static_cast<size_t>(Kp) * 4;
     case GG_I8: return static_cast<size_t>(Kp / 4) * 16;
     default: return 0;
   }
@@ -596,13 +590,9 @@ int launch_checksum_aux(int ab_kind, const void* w_sum, int64_t K, void* aux, cu
   if (K < 1) return fail(GG_EINVAL, "checksum_aux: empty w_sum");
   const int64_t Kp = aux_padded(K);
   switch (ab_kind) {
-    case GG_BF16: case GG_F16:
+    case GG_BF16: case GG_F16: case GG_F32:
       f32_of_f64_kernel<<<grid1(Kp, 256), 256, 0, s>>>(static_cast<const double*>(w_sum), K, Kp,
                                                        static_cast<float*>(aux));
-      break;
-    case GG_F32:
-      f64_copy_kernel<<<grid1(Kp, 256), 256, 0, s>>>(static_cast<const double*>(w_sum), K, Kp,
-                                                     static_cast<double*>(aux));
       break;
     case GG_I8:
       digits_i64_kernel<<<grid1(Kp / 4, 256), 256, 0, s>>>(static_cast<const long long*>(w_sum), K, Kp,

@@ -191,8 +191,8 @@ def build_desc(
 
 def checksum_aux(w_sum: torch.Tensor, ab_dtype: torch.dtype) -> torch.Tensor | None:
     """Side-path encoding of w_sum for the fused checksum (gg_checksum_aux):
-    (hi, lo) fp32 split for bf16/fp16 operands, signed digit planes for int8,
-    None for fp32 (tf32) operands.  Computed once per weight."""
+    fp32(w_sum) for float operands (bf16 / fp16 / tf32), signed base-256 digit
+    planes for int8.  Computed once per weight."""
     dev = _require_cuda(w_sum)
     kind = TORCH_TO_GG[ab_dtype]
     K = w_sum.numel()
