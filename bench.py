@@ -238,8 +238,22 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                 launch(ly, protect)
         return graph
 
-    g_prot = capture(True)
-    g_unprot = capture(False)
+    if args.eager:  # eager launches (programmatic dependent launch overlaps consecutive kernels)
+        class _Eager:
+            def __init__(self, protect):
+                self.protect = protect
+
+            def replay(self):
+                for ly in layers:
+                    launch(ly, self.protect)
+        for ly in layers:
+            launch(ly, True)
+            launch(ly, False)
+        torch.cuda.synchronize()
+        g_prot, g_unprot = _Eager(True), _Eager(False)
+    else:
+        g_prot = capture(True)
+        g_unprot = capture(False)
     stream = torch.cuda.current_stream(dev)
 
     def timed(graph, steps, warmup):
@@ -390,6 +404,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--ref-rows", type=int, default=TOKENS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="time eager launches instead of one CUDA graph per step")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
