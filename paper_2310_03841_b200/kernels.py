@@ -277,6 +277,52 @@ def protected_gemm(
     return y, (result if protect else None)
 
 
+def packed_output_campaign(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    bias: torch.Tensor | None,
+    faults: Sequence[Injection],
+    *,
+    w_sum: torch.Tensor,
+    w_aux: torch.Tensor | None = None,
+    bias_sum: float | int = 0,
+    mu: float = 0.0,
+    lo: float = 0.0,
+    hi: float = 0.0,
+) -> tuple[torch.Tensor, int]:
+    """Campaign engine for independent single-fault trials on one layer input:
+    fault i is detected iff its row is flagged by a launch that injects it.
+
+    The check is per row (guard.py:188-215), so faults in distinct rows do not
+    interact. They are packed greedily into as few protected launches as there
+    are faults per row. Returns (detected [len(faults)] bool on the device,
+    number of launches); the verdicts equal one launch per fault."""
+    dev = _require_cuda(x, w, bias)
+    groups: list[list[int]] = []
+    used: list[set[int]] = []
+    for i, f in enumerate(faults):
+        for g, u in zip(groups, used):
+            if f.row not in u:
+                u.add(f.row)
+                g.append(i)
+                break
+        else:
+            groups.append([i])
+            used.append({f.row})
+    detected = torch.zeros(len(faults), dtype=torch.bool, device=dev)
+    M = x.shape[0]
+    res = CheckResult.empty(M, x.dtype == torch.int8, dev)
+    y = torch.empty((M, w.shape[0]), dtype=default_out_dtype(x.dtype), device=dev)
+    for g in groups:
+        inj = injections_to_device([faults[i] for i in g], dev)
+        protected_gemm(x, w, bias, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi, injections=inj,
+                       out=y, result=res)
+        idx = torch.tensor(g, dtype=torch.int64, device=dev)
+        rows = torch.tensor([faults[i].row for i in g], dtype=torch.int64, device=dev)
+        detected[idx] = res.flags[rows].bool()
+    return detected, len(groups)
+
+
 def replay_tiles(
     x: torch.Tensor,
     w: torch.Tensor,

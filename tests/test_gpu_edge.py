@@ -150,3 +150,22 @@ def test_concurrent_streams_same_shape_do_not_share_counters():
         assert torch.equal(ya, ref1) and torch.equal(yb, ref2)
         assert torch.equal(ra.d, d1) and torch.equal(rb.d, d2)
         assert int(ra.nflag.item()) == 0 and int(rb.nflag.item()) == 0
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.int8])
+def test_packed_output_campaign_equals_one_launch_per_fault(dtype):
+    M, N, Kd = 512, 384, 256
+    x, w, b, ws, bs = _ops(M, N, Kd, dtype, 33)
+    _, r0 = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
+    torch.cuda.synchronize()
+    thr = 0.0 if dtype == torch.int8 else 4 * float(r0.d.abs().max().item())
+    rng = np.random.default_rng(8)
+    faults = [K.Injection(row=int(rng.integers(0, M)), col=int(rng.integers(0, N)), bit=int(rng.integers(0, 15)))
+              for _ in range(400)]  # repeated rows force several launches
+    got, launches = K.packed_output_campaign(x, w, b, faults, w_sum=ws, bias_sum=bs, lo=-thr, hi=thr)
+    assert 1 < launches < 20
+    want = []
+    for f in faults:
+        _, r = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-thr, hi=thr, injections=[f])
+        want.append(bool(r.flags[f.row].item()))
+    assert got.cpu().tolist() == want
