@@ -514,6 +514,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int q = 0; q < 4; ++q) bo[q] = acc_add<OBS_MODE>(b0[q], b1[q]);
   };
+  // The same fold from one burst of async copies into this CTA's pipeline stages, for
+  // launches with at most one tile per pair (a band's finisher CTA has no tile in flight):
+  // one round trip instead of n_tiles / FB.  Layout [tile][half 0, half 1, pred][128 rows].
+  const bool burst_fold = p.one_tile && 3 * n_tiles * BM * 8 <= STAGES * (A_BYTES + B_BYTES);
+  auto fold_band_burst = [&](int b, unsigned long long (&bo)[4], unsigned long long (&bpr)[4]) {
+    const uint32_t sbuf = smem_u32(smA);
+    for (int tt = 0; tt < n_tiles; ++tt) {
+      const size_t g = static_cast<size_t>(tt) * p.m_pad + b * BM + 2 * lane;
+      const uint32_t d0 = sbuf + static_cast<uint32_t>(tt * 3 * BM * 8 + lane * 16);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // rows 2*lane + 64h .. +1
+        cp_async16(d0 + h * 512, gpart + g + 64 * h);
+        cp_async16(d0 + BM * 8 + h * 512, gpart + half_stride + g + 64 * h);
+        cp_async16(d0 + 2 * BM * 8 + h * 512, gpred + g + 64 * h);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    const unsigned long long* sv = reinterpret_cast<const unsigned long long*>(smA);
+    unsigned long long b0[4] = {0ull, 0ull, 0ull, 0ull}, b1[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bpr[q] = 0ull;
+    for (int tt = 0; tt < n_tiles; ++tt) {  // ascending tiles per half, as fold_band
+      const unsigned long long* base = sv + static_cast<size_t>(tt * 3) * BM;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        b0[q] = acc_add<OBS_MODE>(b0[q], base[lane + 32 * q]);
+        b1[q] = acc_add<OBS_MODE>(b1[q], base[BM + lane + 32 * q]);
+        bpr[q] = acc_add<PRED_MODE>(bpr[q], base[2 * BM + lane + 32 * q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bo[q] = acc_add<OBS_MODE>(b0[q], b1[q]);
+    __syncwarp();
+  };
+
   // warp roles; the SMSP arbiter issues highest-warp-id first, so the ids follow criticality
   constexpr int W_MMA = 15, W_PRODUCER = 14, W_ALLOC = 13, W_REDUCER = 12, W_CHK0 = 8, W_EPI0 = 0;
   if (warp == W_PRODUCER && lane == 0) {
@@ -837,7 +873,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lane == 0) mbar_arrive(&fq_empty[q]);
         if (mb < 0) break;
         unsigned long long bo[4], bpr[4];
-        fold_band(mb, bo, bpr);
+        if (burst_fold) fold_band_burst(mb, bo, bpr);
+        else fold_band(mb, bo, bpr);
         finish(mb, bo, bpr);
       }
     }

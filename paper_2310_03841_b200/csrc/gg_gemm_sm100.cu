@@ -349,6 +349,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   if (replay) p.sched = 1;  // replay walks the listed band pairs strided; every band folds via the workspace
   // tiny launches (at most one tile per pair, few bands): one launch-wide fold from smem
   p.tiny = (pair_tiles <= pairs && p.m_tiles <= 4 && p.m_tiles * p.n_tiles <= 48) ? 1 : 0;
+  p.one_tile = (pair_tiles <= pairs && !replay) ? 1 : 0;
 
   switch (kind) {
     case K_BF16:

@@ -169,3 +169,29 @@ def test_packed_output_campaign_equals_one_launch_per_fault(dtype):
         _, r = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-thr, hi=thr, injections=[f])
         want.append(bool(r.flags[f.row].item()))
     assert got.cpu().tolist() == want
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.int8])
+@pytest.mark.parametrize("shape", [(1024, 3072, 768), (512, 8192, 256)])
+def test_one_tile_per_pair_launch_burst_fold(dtype, shape):
+    """At most one tile per CTA pair but more than four bands: every band is split
+    and its finisher folds the partials from one burst into the idle stages.  Faults
+    in several bands are flagged exactly, and replay restores the clean bytes."""
+    M, N, Kd = shape
+    x, w, b, ws, bs = _ops(M, N, Kd, dtype, 41)
+    clean, r0 = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
+    torch.cuda.synchronize()
+    integer = dtype == torch.int8
+    thr = 0.0 if integer else 4 * float(r0.d.abs().max().item()) + 1e-6
+    top = {torch.bfloat16: 14, torch.float32: 30, torch.int8: 30}[dtype]
+    rows = [0, 130, 255, 300, M - 1]
+    y, res = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-thr, hi=thr,
+                              injections=[K.Injection(row=r, col=(37 * r) % N, bit=top) for r in rows])
+    torch.cuda.synchronize()
+    assert torch.nonzero(res.flags.cpu()).flatten().tolist() == rows
+    assert int(res.nflag.item()) == len(rows)
+    changed = K.replay_tiles(x, w, b, y, res.flags, res, w_sum=ws, bias_sum=bs, lo=-thr, hi=thr)
+    torch.cuda.synchronize()
+    assert int(changed.item()) == len(rows)
+    assert torch.equal(y.view(torch.uint8), clean.view(torch.uint8))
+    assert int(res.nflag.item()) == 0
