@@ -83,10 +83,15 @@ constexpr int CST_BYTES = 4096;               // staging per epilogue warp: 2 x 
 constexpr int C_OFF = STAGES * (A_BYTES + B_BYTES);
 constexpr int BAR_OFF = C_OFF + EPI_WARPS * CST_BYTES;
 constexpr int NSLOT = 4;                      // depth of the observed / predicted partial rings
-constexpr int FQ = 4;                         // finisher queue: split bands whose fold the reducer hands off
+// finisher queue: split bands whose fold the reducer hands off.  Deep enough that the
+// reducer never waits on it: a reducer held up here arrives last at its next bands'
+// counters too, which hands it their folds as well (a feedback loop that left single
+// CTAs tens of microseconds behind on long-N shapes).
+constexpr int FQ = 16;
+constexpr int QAREA = (16 + 4 * FQ + 15) / 16 * 16;  // tmem slot + queued band ids
 constexpr int NBAR = 4 * STAGES + 4 + 4 * NSLOT + 2 * FQ;
 constexpr int W_SMEM = 16384;                 // checksum w-vector kept in shared memory when it fits
-constexpr int SMEM_BYTES = BAR_OFF + NBAR * 8 + 32 /*tmem slot, finisher queue*/ + 3 * NSLOT * BM * 8 /*partial rings*/ +
+constexpr int SMEM_BYTES = BAR_OFF + NBAR * 8 + QAREA /*tmem slot, finisher queue*/ + 3 * NSLOT * BM * 8 /*partial rings*/ +
                            2 * BN * 4 /*bias tiles*/ + W_SMEM + 1024 /*align*/;
 
 template <int KIND> struct PairIdesc;
@@ -112,9 +117,8 @@ struct BandRows {
 };
 
 template <bool INT>
-__device__ __forceinline__ BandRows<INT> band_rows(const Params& p, int mb, int lane, const double (&obs_f)[4],
-                                                  const double (&pred_f)[4], const long long (&obs_i)[4],
-                                                  const long long (&pred_i)[4]) {
+__device__ __forceinline__ BandRows<INT> band_rows(const Params& p, int mb, int lane, const unsigned long long (&obs)[4],
+                                                  const unsigned long long (&pred)[4]) {
   const bool per_sample = INT || p.statistic == GG_PER_SAMPLE;
   BandRows<INT> r;
   r.nflag = 0;
@@ -126,18 +130,27 @@ __device__ __forceinline__ BandRows<INT> band_rows(const Params& p, int mb, int 
     r.dbits[q] = 0;
     if (row >= p.M) continue;
     if constexpr (INT) {
-      const long long di = (pred_i[q] + p.bias_sum_i) - obs_i[q];
+      const long long di = (static_cast<long long>(pred[q]) + p.bias_sum_i) - static_cast<long long>(obs[q]);
       r.dbits[q] = static_cast<unsigned long long>(di);
       r.flag[q] = di != 0;
       const unsigned long long mag =
           di < 0 ? 0ull - static_cast<unsigned long long>(di) : static_cast<unsigned long long>(di);
-      const unsigned long long k = gap_key(static_cast<double>(mag));
+      const unsigned long long k = f64_bits_of_u64(mag) + 1ull;  // gap_key(double(|d|))
       r.key = k > r.key ? k : r.key;
     } else {
-      const double dd = (pred_f[q] + p.bias_sum_f) - obs_f[q];
-      r.dbits[q] = static_cast<unsigned long long>(__double_as_longlong(dd));
-      r.flag[q] = !((dd >= p.lo) && (dd <= p.hi));
-      const unsigned long long k = gap_key(fabs(dd - p.mu));
+      // d = (pred + bias) - obs in double-float, one rounding to binary64 (no FP64 instruction)
+      const unsigned long long dd = df_add(df_add(pred[q], p.bias_df), obs[q] ^ 0x8000000080000000ull);
+      const unsigned long long db = f64_bits_of_df_norm(dd);
+      r.dbits[q] = db;
+      const unsigned long long ok = f64_order_key(db);
+      r.flag[q] = f64_bits_nan(db) || ok < p.lo_key || ok > p.hi_key;  // !(lo <= d <= hi)
+      unsigned long long gb = db & 0x7fffffffffffffffull;                // |d - mu|
+      if (!p.mu_zero) {
+        unsigned long long g = df_add(dd, p.neg_mu_df);
+        if (static_cast<uint32_t>(g) >> 31) g ^= 0x8000000080000000ull;
+        gb = f64_bits_of_df_norm(g);
+      }
+      const unsigned long long k = f64_bits_nan(gb) ? 0ull : gb + 1ull;  // gap_key
       r.key = k > r.key ? k : r.key;
     }
     if (per_sample) r.nflag += r.flag[q] ? 1 : 0;
@@ -192,13 +205,13 @@ __device__ void publish_summary(const Params& p, int lane, int nf, unsigned long
 // d / flags of band mb, its band summary and, for the band that completes the launch's
 // count, the launch summaries (nflag, triggered, max_disc).  One warp.
 template <bool INT>
-__device__ void finish_band(const Params& p, int mb, int lane, const double (&obs_f)[4], const double (&pred_f)[4],
-                            const long long (&obs_i)[4], const long long (&pred_i)[4]) {
+__device__ void finish_band(const Params& p, int mb, int lane, const unsigned long long (&obs)[4],
+                            const unsigned long long (&pred)[4]) {
 #ifdef GG_TRACE
   const long long fb_t0 = clock64();
 #endif
   const bool bmean = !INT && p.statistic == GG_BATCH_MEAN;
-  const BandRows<INT> r = band_rows<INT>(p, mb, lane, obs_f, pred_f, obs_i, pred_i);
+  const BandRows<INT> r = band_rows<INT>(p, mb, lane, obs, pred);
 #ifdef GG_TRACE
   const long long fb_t1 = clock64();
 #endif
@@ -212,7 +225,7 @@ __device__ void finish_band(const Params& p, int mb, int lane, const double (&ob
   }
   int last = 0;
   unsigned long long fin_rows = 0, fin_key = 0;
-  if (lane == 0) {
+  if (lane == 0 && !GG_DBG(8192)) {
     const int total = p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles;
     atomicMax(&p.ws.summary[1], r.key);
     const unsigned long long inc = (1ull << 32) | static_cast<unsigned>(r.nflag);
@@ -254,37 +267,16 @@ __device__ __forceinline__ void two_sum_acc(float& hi, float& lo, float x) {
   hi = t;
 }
 
-// Partial sums travel as 8-byte values in one of three representations (ring slots,
-// workspace partials, reducer accumulators): int64 (int8 operands), an fp32 (hi, lo)
-// double-float pair (16-bit operand / output paths: no FP64 instruction per tile, whose
-// issue is slow next to the tensor pipe), or fp64 (fp32 paths).
-enum { ACC_I64 = 0, ACC_DF = 1, ACC_F64 = 2 };
+// Partial sums travel as 8-byte values (ring slots, workspace partials, reducer
+// accumulators): int64 for int8 operands, else an fp32 (hi, lo) double-float pair -- no
+// FP64 instruction anywhere in the kernel, whose issue is slow next to the tensor pipe.
+enum { ACC_I64 = 0, ACC_DF = 1 };
 template <int MODE>
 __device__ __forceinline__ unsigned long long acc_add(unsigned long long a, unsigned long long b) {
-  if constexpr (MODE == ACC_I64) {
+  if constexpr (MODE == ACC_I64)
     return static_cast<unsigned long long>(static_cast<long long>(a) + static_cast<long long>(b));
-  } else if constexpr (MODE == ACC_DF) {  // (ah, al) + (bh, bl), relative error ~2^-44
-    const float ah = __uint_as_float(static_cast<uint32_t>(a)), al = __uint_as_float(static_cast<uint32_t>(a >> 32));
-    const float bh = __uint_as_float(static_cast<uint32_t>(b)), bl = __uint_as_float(static_cast<uint32_t>(b >> 32));
-    const float sh = ah + bh, bp = sh - ah;
-    float e = (ah - (sh - bp)) + (bh - bp);
-    e += al + bl;
-    const float h = sh + e, l = e - (h - sh);
-    return static_cast<unsigned long long>(__float_as_uint(h)) |
-           (static_cast<unsigned long long>(__float_as_uint(l)) << 32);
-  } else {
-    return static_cast<unsigned long long>(
-        __double_as_longlong(__longlong_as_double(static_cast<long long>(a)) +
-                             __longlong_as_double(static_cast<long long>(b))));
-  }
-}
-template <int MODE>
-__device__ __forceinline__ double acc_f64(unsigned long long a) {
-  if constexpr (MODE == ACC_DF)
-    return static_cast<double>(__uint_as_float(static_cast<uint32_t>(a))) +
-           static_cast<double>(__uint_as_float(static_cast<uint32_t>(a >> 32)));
   else
-    return __longlong_as_double(static_cast<long long>(a));
+    return df_add(a, b);
 }
 
 // 16 bytes of the checksum w-vector encoding at byte offset `off`: an explicit
@@ -413,7 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* fq_empty = fq_full + FQ;            // [FQ] taken by the finisher warp
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fq_empty + FQ);
   int* fq_band = reinterpret_cast<int*>(tmem_slot + 4);           // [FQ]
-  double* slot_obs = reinterpret_cast<double*>(tmem_slot + 8);  // [NSLOT][2 halves][BM] (int64 bits for INT)
+  double* slot_obs = reinterpret_cast<double*>(tmem_slot + QAREA / 4);  // [NSLOT][2 halves][BM] (int64 bits for INT)
   double* slot_pred = slot_obs + 2 * NSLOT * BM;                // [NSLOT][BM]
   uint32_t* bias_sm = reinterpret_cast<uint32_t*>(slot_pred + NSLOT * BM);  // [2][BN] bias of a tile
   uint8_t* w_sm = reinterpret_cast<uint8_t*>(bias_sm + 2 * BN);              // [W_SMEM] checksum w-vector
@@ -464,16 +456,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   unsigned long long* gpred = reinterpret_cast<unsigned long long*>(p.ws.pred);
   // d / flags of a folded band (one conversion to fp64 per row and band)
   auto finish = [&](int mb, const unsigned long long (&ao)[4], const unsigned long long (&ap)[4]) {
-    double of[4], pf[4];
-    long long oi[4], pi[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      oi[q] = static_cast<long long>(ao[q]);
-      pi[q] = static_cast<long long>(ap[q]);
-      of[q] = INT ? 0.0 : acc_f64<OBS_MODE>(ao[q]);
-      pf[q] = INT ? 0.0 : acc_f64<PRED_MODE>(ap[q]);
-    }
-    finish_band<INT>(p, mb, lane, of, pf, oi, pi);
+    finish_band<INT>(p, mb, lane, ao, ap);
   };
   // workspace partials of split bands: observed per column half ([half][tile][row]) and predicted
   const size_t half_stride = static_cast<size_t>(n_tiles) * p.m_pad;
@@ -773,14 +756,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             int last = 0;
             if (lane == 0) {
               const int total = p.tiny ? n_tiles * (p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles) : n_tiles;
-              last = (atom_add_release_gpu(counter, part) == total - part) ? 1 : 0;
+              const int prev = GG_DBG(16) ? atomicAdd(counter, part) : atom_add_release_gpu(counter, part);
+              last = (prev == total - part) ? 1 : 0;
               if (last) {
                 fence_acquire_gpu();  // the other pairs' partials
                 *counter = 0;
               }
             }
             last = __shfl_sync(0xffffffffu, last, 0);
-            if (last && !p.tiny) {  // hand the fold to the finisher warp: the reducer keeps draining slots
+            if (last && !p.tiny && !GG_DBG(32)) {  // hand the fold to the finisher warp: the reducer keeps draining slots
               if (lane == 0) {
                 const int q = fq_i % FQ;
                 mbar_wait(&fq_empty[q], (static_cast<uint32_t>(fq_i / FQ) & 1u) ^ 1u);
@@ -788,7 +772,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 mbar_arrive(&fq_full[q]);
               }
               ++fq_i;
-            } else if (last) {
+            } else if (last && p.tiny) {
               // every band's partials in one burst of async copies into this CTA's (now idle)
               // pipeline stages: [band][tile][obs half 0, obs half 1, pred][128 rows]
               // (m_tiles * n_tiles <= 48)
@@ -832,16 +816,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) bo[q] = acc_add<OBS_MODE>(b0[q], b1[q]);
-                double of[4], pf[4];
-                long long oi[4], pi[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  oi[q] = static_cast<long long>(bo[q]);
-                  pi[q] = static_cast<long long>(bpr[q]);
-                  of[q] = INT ? 0.0 : acc_f64<OBS_MODE>(bo[q]);
-                  pf[q] = INT ? 0.0 : acc_f64<PRED_MODE>(bpr[q]);
-                }
-                const BandRows<INT> r = band_rows<INT>(p, b, lane, of, pf, oi, pi);
+                const BandRows<INT> r = band_rows<INT>(p, b, lane, bo, bpr);
                 store_band<INT>(p, b, lane, r);
                 nf += r.nflag;
                 mk = r.key > mk ? r.key : mk;
@@ -875,7 +850,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         unsigned long long bo[4], bpr[4];
         if (burst_fold) fold_band_burst(mb, bo, bpr);
         else fold_band(mb, bo, bpr);
-        finish(mb, bo, bpr);
+        if (!GG_DBG(256)) finish(mb, bo, bpr);
       }
     }
   } else if (warp >= W_EPI0 && warp < W_EPI0 + EPI_WARPS) {

@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -15,6 +16,22 @@
 namespace gg {
 
 namespace {
+
+unsigned long long f64_bits_host(double x) {
+  unsigned long long b;
+  std::memcpy(&b, &x, sizeof b);
+  return b;
+}
+
+// x as an fp32 (hi, lo) pair, hi in the low word (the kernels' double-float format)
+unsigned long long df_split(double x) {
+  const float h = static_cast<float>(x);
+  const float l = std::isfinite(h) ? static_cast<float>(x - static_cast<double>(h)) : 0.0f;
+  uint32_t uh, ul;
+  std::memcpy(&uh, &h, sizeof uh);
+  std::memcpy(&ul, &l, sizeof ul);
+  return static_cast<unsigned long long>(uh) | (static_cast<unsigned long long>(ul) << 32);
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -305,6 +322,11 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.mu = d->mu;
   p.lo = d->lo;
   p.hi = d->hi;
+  p.bias_df = df_split(d->bias_sum_f);
+  p.neg_mu_df = df_split(-d->mu);
+  p.mu_zero = d->mu == 0.0 ? 1 : 0;
+  p.lo_key = std::isnan(d->lo) ? ~0ull : f64_order_key(f64_bits_host(d->lo));  // NaN bounds: every row flags
+  p.hi_key = std::isnan(d->hi) ? 0ull : f64_order_key(f64_bits_host(d->hi));
   p.statistic = d->statistic;
   p.d = d->d;
   p.flags = d->flags;

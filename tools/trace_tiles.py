@@ -1,7 +1,7 @@
 """Per-tile role timeline of one protected GEMM from the GG_TRACE library.
 
     GEMMGUARD_LIB=paper_2310_03841_b200/_build/libgemmguard_b200_trace.so \
-        python tools/trace_tiles.py M N K [protect]
+        python tools/trace_tiles.py M N K [protect] [bf16|f16|tf32]
 """
 import ctypes, os, sys
 import numpy as np
@@ -10,10 +10,11 @@ sys.path.insert(0, '.')
 from paper_2310_03841_b200 import kernels as K, _lib as L
 M, N, Kd = [int(v) for v in sys.argv[1:4]]
 protect = (sys.argv[4] != '0') if len(sys.argv) > 4 else True
-x = torch.randn(M, Kd, device='cuda').to(torch.bfloat16); w = (torch.randn(N, Kd, device='cuda') / Kd**.5).to(torch.bfloat16)
+dt = {'bf16': torch.bfloat16, 'f16': torch.float16, 'tf32': torch.float32}[sys.argv[5] if len(sys.argv) > 5 else 'bf16']
+x = torch.randn(M, Kd, device='cuda').to(dt); w = (torch.randn(N, Kd, device='cuda') / Kd**.5).to(dt)
 b = torch.zeros(N, device='cuda')
-ws, bs = K.offline_checksum(w, b, L.GG_P_F64); aux = K.checksum_aux(ws, torch.bfloat16); bsv = bs.item()
-y = torch.empty(M, N, dtype=torch.bfloat16, device='cuda'); res = K.CheckResult.empty(M, False, 'cuda')
+ws, bs = K.offline_checksum(w, b, L.GG_P_F64); aux = K.checksum_aux(ws, dt); bsv = bs.item()
+y = torch.empty(M, N, dtype=K.default_out_dtype(dt), device='cuda'); res = K.CheckResult.empty(M, False, 'cuda')
 lib = L.load(); lib.gg_trace_buffer.argtypes = [ctypes.c_void_p]
 TT, EV = 64, 28
 buf = torch.zeros(148 * TT * EV + 4 * 64 * 4, dtype=torch.int64, device='cuda')
@@ -93,3 +94,15 @@ if fc:
     a = np.array(fc)
     print('last band finish (median cycles): d/flags compute', np.median(a[:, 0]), 'summary atomics', np.median(a[:, 1]),
           'row stores', np.median(a[:, 2]))
+
+# the CTA with the longest reducer tail: its last tiles, relative to that tile's epilogue end
+if tails:
+    worst = [c for c in range(148) if any(t[c, i, 2] > 0 and t[c, i, 9] > 0 for i in range(TT))]
+    wc = worst[int(np.argmax(tails))]
+    r = t[wc]
+    idx = [i for i in range(TT) if r[i, 2] > 0 and r[i, 9] > 0]
+    ref = r[idx[-1], 2]
+    print(f'worst tail: CTA {wc}, tiles {len(idx)}; events relative to its last epilogue end')
+    for i in idx[-4:]:
+        f = lambda e: int(r[i, e] - ref) if r[i, e] > 0 else None
+        print(f'  tile {i:2d}: epi done {f(2)} | chk done {f(6)} slot {f(7)} | red wait {f(11)} obs {f(12)} got {f(8)} done {f(9)}')
