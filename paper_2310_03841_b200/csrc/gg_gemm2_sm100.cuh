@@ -384,6 +384,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   constexpr bool PRED_PAIR = !INT;  // float kinds: predicted partials as an fp32 (hi, lo) pair
   constexpr int OBS_MODE = INT ? ACC_I64 : ACC_DF;
   constexpr int PRED_MODE = INT ? ACC_I64 : ACC_DF;
+  // Split-band folds: claimed in order by every CTA's finisher (tf32) or handed to the
+  // finisher of the band's last arriver (the other kinds).  With tf32's long tiles a pair
+  // that is slightly late is the last arriver of a band in almost every wave, and its
+  // finisher backlog (a fold takes longer than a tile) made it later still; claiming
+  // spreads the folds over all SMs (tf32 ViT-B fc1: 30% -> 11% overhead).  The other
+  // kinds keep the local hand-off: the claim loop's code shifts their hot loops'
+  // register allocation (the 128-register cap) and costs them more than it saves.
+  // Only where a fold outlasts a tile: bands of >= 8 tiles (fewer fold in <= 2 round
+  // trips, and claiming costs them ~5%).  One-tile launches keep the hand-off for every
+  // kind: there the last arriver's burst fold from its idle stages is the shortest path.
+  constexpr bool CLAIM_KIND = KIND == K_TF32;
+  const bool claim = CLAIM_KIND && !p.one_tile && p.n_tiles >= 8;
   constexpr uint32_t IDESC = PairIdesc<KIND>::V;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -757,7 +769,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if (lane == 0) {
               const int total = p.tiny ? n_tiles * (p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles) : n_tiles;
               const int prev = GG_DBG(16) ? atomicAdd(counter, part) : atom_add_release_gpu(counter, part);
-              last = (prev == total - part) ? 1 : 0;
+              // claim mode: only a tiny launch's last tile acts; the claimed band's finisher
+              // waits for its count to reach n_tiles (one release sequence) and resets it
+              last = ((!claim || p.tiny) && prev == total - part) ? 1 : 0;
               if (last) {
                 fence_acquire_gpu();  // the other pairs' partials
                 *counter = 0;
@@ -839,7 +853,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else if (warp == W_ALLOC) {
     // ================================================= finisher: folds and finishes split bands
     // handed off by the reducer (acquire ordering: the reducer's fence, then this barrier)
-    if constexpr (PROTECT) {
+    if (PROTECT && claim) {
+      // Every CTA's finisher claims the launch's split bands in order from one counter and
+      // folds each once its count is complete.  Claim lists: strided -- every band;
+      // contiguous -- the bands cut by a pair-range boundary; replay -- the active bands.
+      if (!p.tiny && !GG_DBG(4) && !GG_DBG(128)) {  // (those diagnostics count no band)
+        const int n_claims = p.replay ? 2 * __ldcg(&p.ws.counters[2]) : p.sched ? p.m_tiles : 2 * (npairs - 1);
+        for (;;) {
+          int idx = 0;
+          if (lane == 0) idx = atomicAdd(&p.ws.counters[0], 1);
+          idx = __shfl_sync(0xffffffffu, idx, 0);
+          if (idx >= n_claims) {  // the launch's last claim leaves the counter ready
+            if (lane == 0 && idx == n_claims + static_cast<int>(gridDim.x) - 1) p.ws.counters[0] = 0;
+            break;
+          }
+          int mb;
+          if (p.replay) {
+            mb = 2 * __ldcg(&p.ws.active_pairs[idx >> 1]) + (idx & 1);
+            if (mb >= p.m_tiles || !p.ws.band_active[mb]) continue;
+          } else if (p.sched) {
+            mb = idx;
+          } else {  // the boundary between pairs bp - 1 and bp; one claim per cut band
+            int ta, tb, ua, ub;
+            const int bp = (idx >> 1) + 1;
+            pair_range(bp, npairs, m_pairs * n_tiles, ta, tb);
+            if (ta % n_tiles == 0) continue;
+            pair_range(bp - 1, npairs, m_pairs * n_tiles, ua, ub);
+            if (ua % n_tiles != 0 && ua / n_tiles == ta / n_tiles) continue;
+            mb = 2 * (ta / n_tiles) + (idx & 1);
+            if (mb >= p.m_tiles) continue;
+          }
+          if (lane == 0) {  // relaxed polls (no L1 invalidation), then one acquire
+            while (ld_relaxed_gpu(&p.ws.band_counter[mb]) != n_tiles) __nanosleep(256);
+            fence_acquire_gpu();
+          }
+          __syncwarp();
+          unsigned long long bo[4], bpr[4];
+          fold_band(mb, bo, bpr);
+          finish(mb, bo, bpr);
+          __syncwarp();
+          if (lane == 0) p.ws.band_counter[mb] = 0;
+        }
+      }
+    } else if constexpr (PROTECT) {
       for (int i = 0;; ++i) {
         const int q = i % FQ;
         mbar_wait(&fq_full[q], static_cast<uint32_t>(i / FQ) & 1u);

@@ -106,7 +106,7 @@ def test_replay_with_nothing_flagged_keeps_outputs_and_summary():
     assert float(res.max_disc.item()) == md
 
 
-@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.int8])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.int8])
 def test_replay_under_strided_schedule_at_scale(dtype):
     """M = 50432, K = 3072: the long-K shape walks tiles strided and every band
     folds through the workspace; faults in three bands are detected, replayed,
@@ -118,6 +118,10 @@ def test_replay_under_strided_schedule_at_scale(dtype):
     thr = 0.0 if integer else 4 * float(r0.d.abs().max().item())
     top = 14 if dtype == torch.bfloat16 else 30
     rows = [5, 25000, M - 1]
+    if dtype == torch.float32:
+        _, r1 = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
+        torch.cuda.synchronize()
+        assert torch.equal(r1.d.view(torch.int64), r0.d.view(torch.int64))  # claimed folds: same association
     y, res = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-thr, hi=thr,
                               injections=[K.Injection(row=r, col=100 + r % 500, bit=top) for r in rows])
     torch.cuda.synchronize()

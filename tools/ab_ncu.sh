@@ -4,7 +4,7 @@
 shape=$1; shift
 for v in "$@"; do
   if [ "$v" != cur ]; then export GEMMGUARD_LIB=paper_2310_03841_b200/_build/libgemmguard_b200_$v.so; else unset GEMMGUARD_LIB; fi
-  ncu --metrics gpu__time_duration.sum -k regex:gg_protected --csv python tools/prof_one.py $shape bf16 2>/dev/null \
+  ncu --metrics gpu__time_duration.sum -k regex:gg_protected --csv python tools/prof_one.py $shape ${DT:-bf16} 2>/dev/null \
     | python -c "
 import sys, csv
 rows = list(csv.reader(sys.stdin)); h = next(r for r in rows if 'Kernel Name' in r); K = h.index('Kernel Name'); V = h.index('Metric Value')

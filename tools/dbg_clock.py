@@ -5,10 +5,11 @@ import pynvml
 sys.path.insert(0, '.')
 from paper_2310_03841_b200 import kernels as K, _lib as L
 M, N, Kd = [int(v) for v in sys.argv[1:4]]
-x = torch.randn(M, Kd, device='cuda').to(torch.bfloat16); w = (torch.randn(N, Kd, device='cuda') / Kd**.5).to(torch.bfloat16)
+dt = {'bf16': torch.bfloat16, 'f16': torch.float16, 'tf32': torch.float32}[sys.argv[4] if len(sys.argv) > 4 else 'bf16']
+x = torch.randn(M, Kd, device='cuda').to(dt); w = (torch.randn(N, Kd, device='cuda') / Kd**.5).to(dt)
 b = torch.zeros(N, device='cuda')
-ws, bs = K.offline_checksum(w, b, L.GG_P_F64); aux = K.checksum_aux(ws, torch.bfloat16); bsv = bs.item()
-y = torch.empty(M, N, dtype=torch.bfloat16, device='cuda'); res = K.CheckResult.empty(M, False, 'cuda')
+ws, bs = K.offline_checksum(w, b, L.GG_P_F64); aux = K.checksum_aux(ws, dt); bsv = bs.item()
+y = torch.empty(M, N, dtype=K.default_out_dtype(dt), device='cuda'); res = K.CheckResult.empty(M, False, 'cuda')
 pynvml.nvmlInit(); h = pynvml.nvmlDeviceGetHandleByIndex(0)
 def t(fn):
     for _ in range(5): fn()

@@ -3,7 +3,7 @@ import sys, torch
 sys.path.insert(0, '.')
 from paper_2310_03841_b200 import kernels as K, _lib as L
 M, N, Kd = [int(v) for v in (sys.argv[1:4] if len(sys.argv) > 3 else (50432, 768, 3072))]
-dt = {'bf16': torch.bfloat16, 'i8': torch.int8}[sys.argv[4] if len(sys.argv) > 4 else 'bf16']
+dt = {'bf16': torch.bfloat16, 'i8': torch.int8, 'f16': torch.float16, 'tf32': torch.float32}[sys.argv[4] if len(sys.argv) > 4 else 'bf16']
 if dt == torch.int8:
     x = torch.randint(-128, 128, (M, Kd), dtype=torch.int8, device='cuda'); w = torch.randint(-128, 128, (N, Kd), dtype=torch.int8, device='cuda'); b = torch.zeros(N, dtype=torch.int32, device='cuda'); prec = L.GG_P_I64
 else:

@@ -106,3 +106,14 @@ if tails:
     for i in idx[-4:]:
         f = lambda e: int(r[i, e] - ref) if r[i, e] > 0 else None
         print(f'  tile {i:2d}: epi done {f(2)} | chk done {f(6)} slot {f(7)} | red wait {f(11)} obs {f(12)} got {f(8)} done {f(9)}')
+
+# per-CTA span (one SM clock each): first event to the last reducer / epilogue event
+spans = []
+for cta in range(148):
+    r = t[cta]
+    ev = r[:, :13][r[:, :13] > 0]
+    if ev.size: spans.append((int(ev.max() - ev.min()), cta, int((r[:, 0] > 0).sum())))
+if spans:
+    s = sorted(spans)
+    print('per-CTA span (cycles): min', s[0], 'median', s[len(s) // 2], 'max', s[-1])
+    print('  longest 6:', s[-6:])
