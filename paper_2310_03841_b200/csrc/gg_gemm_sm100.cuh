@@ -167,7 +167,8 @@ __device__ __forceinline__ unsigned long long f64_bits_of_u64(unsigned long long
 }
 
 // hi + lo of an fp32 pair, rounded once to binary64 (exact whenever it fits 53 bits).
-__device__ __forceinline__ unsigned long long f64_bits_of_df(unsigned long long df) {
+// Out of line: the rare general case of f64_bits_of_df_norm (one copy, not one per row).
+__device__ __noinline__ unsigned long long f64_bits_of_df(unsigned long long df) {
   const uint32_t uh = static_cast<uint32_t>(df), ul = static_cast<uint32_t>(df >> 32);
   const uint32_t eh = (uh >> 23) & 0xffu, el = (ul >> 23) & 0xffu;
   if (eh == 0xffu || el == 0xffu) return f64_bits_of_f32(__float_as_uint(__uint_as_float(uh) + __uint_as_float(ul)));
