@@ -50,7 +50,7 @@ CONFIDENCE = 1.0 - 1e-9  # per-row checks: ~50k rows x 50 layers per step => kee
 
 # DRAM bytes (read + write) per protected launch, from `ncu --set full` captures of
 # this kernel (profiles/r01/ncu_full_bf16_vitb.json; profiles/ does not travel to the box)
-NCU_DRAM_MB = {"qkv": 284.8, "proj": 114.5, "fc1": 368.5, "fc2": 387.3}  # protected launches, ncu --set full (profiles/r01)
+NCU_DRAM_MB = {"qkv": 282.1, "proj": 116.5, "fc1": 371.7, "fc2": 382.4}  # protected launches, ncu --set full (profiles/r01)
 
 
 def step_traffic_bytes() -> float:
