@@ -371,7 +371,7 @@ __device__ __forceinline__ void stage_row(uint32_t box, int lane, const uint32_t
   }
 }
 
-template <int KIND, int OUT, bool PROTECT>
+template <int KIND, int OUT, bool PROTECT, bool CLAIM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gg_protected_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                   const __grid_constant__ CUtensorMap tmC, const Params p) {
@@ -384,18 +384,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   constexpr bool PRED_PAIR = !INT;  // float kinds: predicted partials as an fp32 (hi, lo) pair
   constexpr int OBS_MODE = INT ? ACC_I64 : ACC_DF;
   constexpr int PRED_MODE = INT ? ACC_I64 : ACC_DF;
-  // Split-band folds: claimed in order by every CTA's finisher (tf32) or handed to the
-  // finisher of the band's last arriver (the other kinds).  With tf32's long tiles a pair
-  // that is slightly late is the last arriver of a band in almost every wave, and its
-  // finisher backlog (a fold takes longer than a tile) made it later still; claiming
-  // spreads the folds over all SMs (tf32 ViT-B fc1: 30% -> 11% overhead).  The other
-  // kinds keep the local hand-off: the claim loop's code shifts their hot loops'
-  // register allocation (the 128-register cap) and costs them more than it saves.
-  // Only where a fold outlasts a tile: bands of >= 8 tiles (fewer fold in <= 2 round
-  // trips, and claiming costs them ~5%).  One-tile launches keep the hand-off for every
-  // kind: there the last arriver's burst fold from its idle stages is the shortest path.
-  constexpr bool CLAIM_KIND = KIND == K_TF32;
-  const bool claim = CLAIM_KIND && !p.one_tile && p.n_tiles >= 8;
+  // Split-band folds: claimed in order by every CTA's finisher (CLAIM) or handed to the
+  // finisher of the band's last arriver.  The launcher claims for tf32 launches with bands
+  // of >= 8 tiles and more than one tile per pair: there a pair that is slightly late is
+  // the last arriver of a band in almost every wave, and its finisher backlog (a fold
+  // outlasts a tile) made it later still; claiming spreads the folds over all SMs (tf32
+  // ViT-B fc1: 30% -> 11% overhead).  A separate instantiation, because compiling the
+  // claim loop into a kernel shifts its hot loops' register allocation (128-register cap)
+  // and costs every launch of it 4-10 points, claiming or not.
+  constexpr bool claim = CLAIM;
   constexpr uint32_t IDESC = PairIdesc<KIND>::V;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -853,7 +850,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else if (warp == W_ALLOC) {
     // ================================================= finisher: folds and finishes split bands
     // handed off by the reducer (acquire ordering: the reducer's fence, then this barrier)
-    if (PROTECT && claim) {
+    if constexpr (PROTECT && CLAIM) {
       // Every CTA's finisher claims the launch's split bands in order from one counter and
       // folds each once its count is complete.  Claim lists: strided -- every band;
       // contiguous -- the bands cut by a pair-range boundary; replay -- the active bands.

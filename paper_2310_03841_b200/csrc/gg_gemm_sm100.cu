@@ -182,10 +182,10 @@ __global__ void replay_prepare_kernel(const uint8_t* rows, int M, int m_tiles, u
   }
 }
 
-template <int KIND, int OUT, bool PROTECT>
+template <int KIND, int OUT, bool PROTECT, bool CLAIM = false>
 int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p, int grid,
                          cudaStream_t s) {
-  auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT>;
+  auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT, CLAIM>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES) != cudaSuccess)
@@ -215,8 +215,11 @@ int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
 template <int KIND, int OUT>
 int dispatch_protect(bool protect, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
                      int grid, cudaStream_t s) {
-  return protect ? launch_pair_instance<KIND, OUT, true>(ta, tb, tc, p, grid, s)
-                 : launch_pair_instance<KIND, OUT, false>(ta, tb, tc, p, grid, s);
+  if (!protect) return launch_pair_instance<KIND, OUT, false>(ta, tb, tc, p, grid, s);
+  if constexpr (KIND == K_TF32) {  // claimed split-band folds (see the kernel)
+    if (!p.one_tile && p.n_tiles >= 8) return launch_pair_instance<KIND, OUT, true, true>(ta, tb, tc, p, grid, s);
+  }
+  return launch_pair_instance<KIND, OUT, true>(ta, tb, tc, p, grid, s);
 }
 
 }  // namespace

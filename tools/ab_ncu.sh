@@ -8,8 +8,11 @@ for v in "$@"; do
     | python -c "
 import sys, csv
 rows = list(csv.reader(sys.stdin)); h = next(r for r in rows if 'Kernel Name' in r); K = h.index('Kernel Name'); V = h.index('Metric Value')
-u = [float(r[V].replace(',', '')) for r in rows[rows.index(h) + 1:] if len(r) == len(h) and r[K].rstrip().endswith('0>(CUtensorMap_st, CUtensorMap_st, CUtensorMap_st, Params)')]
-p = [float(r[V].replace(',', '')) for r in rows[rows.index(h) + 1:] if len(r) == len(h) and r[K].rstrip().endswith('1>(CUtensorMap_st, CUtensorMap_st, CUtensorMap_st, Params)')]
+import re
+prot = lambda r: re.search(r'pair_kernel<\\d+, \\d+, (\\d)', r[K]).group(1) == '1'  # <KIND, OUT, PROTECT, CLAIM>
+body = [r for r in rows[rows.index(h) + 1:] if len(r) == len(h) and 'pair_kernel<' in r[K]]
+u = [float(r[V].replace(',', '')) for r in body if not prot(r)]
+p = [float(r[V].replace(',', '')) for r in body if prot(r)]
 print(f'[$v] $shape unprot {sum(u)/len(u)/1e3:.1f}us prot {sum(p)/len(p)/1e3:.1f}us overhead {100*(sum(p)/len(p)/(sum(u)/len(u))-1):.1f}%')
 "
 done
