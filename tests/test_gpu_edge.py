@@ -199,3 +199,29 @@ def test_one_tile_per_pair_launch_burst_fold(dtype, shape):
     assert int(changed.item()) == len(rows)
     assert torch.equal(y.view(torch.uint8), clean.view(torch.uint8))
     assert int(res.nflag.item()) == 0
+
+
+@pytest.mark.parametrize("shape", [(8192, 3072, 768), (50432, 2048, 256)])
+def test_tf32_claimed_folds_replay(shape):
+    """tf32 launches with >= 8 tiles per band fold their split bands through the claimed
+    path (strided and contiguous schedules, and replay's active-band list): faults in
+    several bands are flagged exactly, replay restores the clean bytes, and d repeats."""
+    M, N, Kd = shape
+    x, w, b, ws, bs = _ops(M, N, Kd, torch.float32, 17)
+    clean, r0 = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
+    torch.cuda.synchronize()
+    d0 = r0.d.clone()
+    _, r1 = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
+    torch.cuda.synchronize()
+    assert torch.equal(r1.d.view(torch.int64), d0.view(torch.int64))
+    thr = 4 * float(d0.abs().max().item()) + 1e-6
+    rows = [3, 700, 4100, M - 2]
+    y, res = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-thr, hi=thr,
+                              injections=[K.Injection(row=r, col=(11 * r) % N, bit=30) for r in rows])
+    torch.cuda.synchronize()
+    assert torch.nonzero(res.flags.cpu()).flatten().tolist() == rows
+    changed = K.replay_tiles(x, w, b, y, res.flags, res, w_sum=ws, bias_sum=bs, lo=-thr, hi=thr)
+    torch.cuda.synchronize()
+    assert int(changed.item()) == len(rows)
+    assert torch.equal(y.view(torch.uint8), clean.view(torch.uint8))
+    assert int(res.nflag.item()) == 0

@@ -147,7 +147,7 @@ def test_flip_bits_involution():
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16, torch.float32, torch.int8])
 @pytest.mark.parametrize("shape", [(50432, 768, 768), (50432, 768, 3072), (4096, 3072, 768), (1024, 3072, 768),
-                                   (512, 8192, 256), (50432, 1024, 256)])
+                                   (512, 8192, 256), (50432, 1024, 256), (50432, 2048, 256)])
 def test_fused_check_is_deterministic_and_accurate_at_scale(dtype, shape):
     """Full-size launches (many tiles per CTA pair, split and local bands; contiguous,
     strided and one-tile schedules, and tf32's claimed folds in the first two):
