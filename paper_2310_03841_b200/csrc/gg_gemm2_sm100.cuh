@@ -471,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const size_t half_stride = static_cast<size_t>(n_tiles) * p.m_pad;
   // ascending-tile fold of band b's workspace partials: per half, then the halves (the same
   // association as a band folded where it was computed); FB tiles' loads in flight together
-  constexpr int FB = 2;  // tiles whose loads are in flight together (register budget)
+  constexpr int FB = INT ? 2 : 3;  // tiles whose loads are in flight together (register budget)
   auto fold_band = [&](int b, unsigned long long (&bo)[4], unsigned long long (&bpr)[4]) {
     unsigned long long b0[4], b1[4];
 #pragma unroll
