@@ -135,7 +135,11 @@ GG_API size_t gg_protected_gemm_workspace_bytes(int64_t M, int64_t N);
 /* K1 — protected GEMM (tcgen05 + TMEM + TMA, sm_100a).
  * Replaces numerics.gemm (numerics.py:237-289) + model.run_layer
  * (model.py:334-338) + guard._discrepancies (guard.py:163-171) +
- * guard._verify_arrays (guard.py:188-215) fused in one launch. */
+ * guard._verify_arrays (guard.py:188-215) fused in one launch.
+ * Float kinds: both sides of d accumulate as fp32 (hi, lo) pairs in fixed
+ * orders, and d = (pred + bias_sum_f) - obs is rounded once to binary64 (no FP64
+ * instruction runs in the kernel); |d - fp64 d| <= 2^-19 * sum of |terms|, and
+ * repeated launches and replays give bit-identical d.  Int8: d is exact int64. */
 GG_API int gg_protected_gemm(const gg_gemm_desc* desc, void* stream);
 
 /* K4 — replay only the M-bands holding a row with replay_rows[m] != 0, with
@@ -161,7 +165,7 @@ GG_API int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_
  * 128 K-elements so the kernel reads whole K-blocks:
  *   GG_BF16 / GG_F16: float [Kp]  = fp32(w_sum); bf16/fp16 x are exact in fp32,
  *                     so x*w is one fp32 FMA (|w - w_sum| <= 2^-24 |w_sum|),
- *                     folded into fp64 once per K-block of 64;
+ *                     folded by TwoSum into an fp32 (hi, lo) pair;
  *   GG_F32 (tf32):    float  [Kp] = fp32(w_sum) (as the 16-bit kinds);
  *   GG_I8:            int32x4 [Kp/4] signed base-256 digit planes of the int64
  *                     w_sum (|w_sum| < 2^23), so x*w_sum is an exact IDP4A dot. */
