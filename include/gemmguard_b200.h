@@ -42,7 +42,9 @@ enum gg_dtype {
   GG_BF16 = 3,  /* extension: bfloat16 (fields 7,8) — not in the reference */
   GG_I8 = 4,    /* "int8"                                                  */
   GG_I32 = 5,   /* "int32"                                                 */
-  GG_I64 = 6
+  GG_I64 = 6,
+  GG_TF32X3 = 7 /* operand kind of gg_checksum_aux: fp32 operands run as a
+                   3xTF32 split (gg_split_tf32x3), the default for binary32 */
 };
 
 /* ---- checksum / accumulation precisions (numerics.py:77-111) ------------ */
@@ -167,11 +169,29 @@ GG_API int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_
  *                     so x*w is one fp32 FMA (|w - w_sum| <= 2^-24 |w_sum|),
  *                     folded by TwoSum into an fp32 (hi, lo) pair;
  *   GG_F32 (tf32):    float  [Kp] = fp32(w_sum) (as the 16-bit kinds);
+ *   GG_TF32X3:        float [3*Ks, padded to 128] = [w | 0 | w] over the
+ *                     three segments of a gg_split_tf32x3 expansion (K is the
+ *                     original K; Ks = K rounded up to 32);
  *   GG_I8:            int32x4 [Kp/4] signed base-256 digit planes of the int64
  *                     w_sum (|w_sum| < 2^23), so x*w_sum is an exact IDP4A dot. */
 GG_API size_t gg_checksum_aux_bytes(int32_t ab_kind, int64_t K);
 GG_API int gg_checksum_aux(int32_t ab_kind, const void* w_sum, int64_t K, void* aux_out,
                            void* stream);
+
+/* binary32 at binary32 accuracy on the tf32 tensor pipe (3xTF32).  Expands an
+ * fp32 operand [rows, K] (row pitch ld) into dst [rows, 3*Ks] (row pitch ldd >=
+ * 3*Ks, Ks = K rounded up to 32; pads zero):
+ *   role 0 (A = X): [hi | hi | lo]        role 1 (B = W [N, K]): [hi | lo | hi]
+ * with hi = x rounded to tf32 (RNE) and lo = x - hi (exact in fp32).  A
+ * gg_protected_gemm launch with ab_kind GG_F32 over the expanded operands
+ * (K' = 3*Ks) accumulates hi*hi + hi*lo + lo*hi per product in fp32 — the
+ * binary32 product of numerics.gemm (numerics.py:222-234) to ~2^-21 instead of
+ * tf32's 2^-11 — and, with w_aux = gg_checksum_aux(GG_TF32X3, w_sum, K), its
+ * predicted row sum is (hi + lo) . w = x . w exactly as before.  Non-finite x
+ * are kept whole in the first segment (zeros elsewhere).  Plain single-pass
+ * TF32 stays available as an explicit opt-in (ab_kind GG_F32 on x itself). */
+GG_API int gg_split_tf32x3(const float* src, int64_t rows, int64_t K, int64_t ld, int32_t role,
+                           float* dst, int64_t ldd, void* stream);
 
 /* Reference-exact verification of a given (X, Y): sequential folds in the
  * checksum precision exactly as guard._discrepancies (guard.py:163-171) and

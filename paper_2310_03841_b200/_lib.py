@@ -17,7 +17,7 @@ import os
 LIB_PATH = Path(os.environ.get("GEMMGUARD_LIB", Path(__file__).resolve().parent / "libgemmguard_b200.so"))
 
 # enum gg_dtype
-GG_F64, GG_F32, GG_F16, GG_BF16, GG_I8, GG_I32, GG_I64 = range(7)
+GG_F64, GG_F32, GG_F16, GG_BF16, GG_I8, GG_I32, GG_I64, GG_TF32X3 = range(8)
 # enum gg_precision
 GG_P_F16, GG_P_F32, GG_P_F64, GG_P_I64 = range(4)
 GG_PER_SAMPLE, GG_BATCH_MEAN = 0, 1
@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "gg_replay_tiles",
     "gg_checksum_aux_bytes",
     "gg_checksum_aux",
+    "gg_split_tf32x3",
     "gg_offline_checksum",
     "gg_verify_rows",
     "gg_flip_bits",
@@ -131,6 +132,8 @@ def load(path: Path | None = None):
     lib.gg_checksum_aux.restype = c_int32
     lib.gg_checksum_aux.argtypes = [c_int32, c_void_p, c_int64, c_void_p, c_void_p]
     lib.gg_offline_checksum.restype = c_int32
+    lib.gg_split_tf32x3.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_int32, c_void_p, c_int64, c_void_p]
+    lib.gg_split_tf32x3.restype = c_int32
     lib.gg_offline_checksum.argtypes = [
         c_int32, c_void_p, c_int64, c_int64, c_int64, c_int32, c_void_p, c_int32, c_int32, c_void_p, c_void_p,
         c_void_p,

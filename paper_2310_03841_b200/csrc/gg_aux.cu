@@ -17,6 +17,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <type_traits>
@@ -288,6 +289,86 @@ __device__ double np_pairwise_sum(const double* a, int64_t n) {
   return ret;
 }
 
+// The same sum computed by one block: the recursion's leaves (<= 128 contiguous
+// elements, split points fixed by n alone) are summed by separate threads with
+// the leaf routine above, then thread 0 combines them in the recursion's order,
+// so the result is bit-identical to the serial form.  Falls back to the serial
+// walk when n has more leaves than fit in shared memory.
+constexpr int PW_MAX_LEAVES = 2048;
+__device__ double np_pairwise_sum_block(const double* a, int64_t n) {
+  __shared__ long long s_leaf[PW_MAX_LEAVES];  // off << 8 | len
+  __shared__ double s_val[PW_MAX_LEAVES];
+  __shared__ int s_nleaf;
+  __shared__ double s_res;
+  if (threadIdx.x == 0) {
+    // pre-order walk listing the leaves left to right
+    int64_t st_off[64], st_len[64];
+    int sp = 0, nl = 0;
+    st_off[0] = 0;
+    st_len[0] = n;
+    while (sp >= 0 && nl <= PW_MAX_LEAVES) {
+      const int64_t off = st_off[sp], len = st_len[sp];
+      --sp;
+      if (len <= 128) {
+        if (nl < PW_MAX_LEAVES) s_leaf[nl] = (static_cast<long long>(off) << 8) | len;
+        ++nl;
+        continue;
+      }
+      int64_t n2 = len / 2;
+      n2 -= n2 % 8;
+      st_off[++sp] = off + n2;  // right child popped after the left one
+      st_len[sp] = len - n2;
+      st_off[++sp] = off;
+      st_len[sp] = n2;
+    }
+    s_nleaf = nl;
+  }
+  __syncthreads();
+  const int nl = s_nleaf;
+  if (nl > PW_MAX_LEAVES) {
+    if (threadIdx.x == 0) s_res = np_pairwise_sum(a, n);
+    __syncthreads();
+    return s_res;
+  }
+  for (int i = threadIdx.x; i < nl; i += blockDim.x)
+    s_val[i] = np_pairwise_sum(a + (s_leaf[i] >> 8), s_leaf[i] & 0xff);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // post-order combine: the same tree, leaves consumed in order
+    struct Fr { int64_t len; int state; double left; };
+    Fr st[64];
+    int sp = 0, li = 0;
+    st[0] = {n, 0, 0.0};
+    double ret = 0.0;
+    while (sp >= 0) {
+      Fr& f = st[sp];
+      if (f.len <= 128) {
+        ret = s_val[li++];
+        --sp;
+        continue;
+      }
+      int64_t n2 = f.len / 2;
+      n2 -= n2 % 8;
+      if (f.state == 0) {
+        f.state = 1;
+        st[sp + 1] = {n2, 0, 0.0};
+        ++sp;
+      } else if (f.state == 1) {
+        f.left = ret;
+        f.state = 2;
+        st[sp + 1] = {f.len - n2, 0, 0.0};
+        ++sp;
+      } else {
+        ret = __dadd_rn(f.left, ret);
+        --sp;
+      }
+    }
+    s_res = ret;
+  }
+  __syncthreads();
+  return s_res;
+}
+
 // One block: launch summaries of guard._verify_arrays over all rows
 // (deterministic: integer sum / max of order-preserving keys).
 __global__ void verify_finish_kernel(int64_t M, bool is_int, int statistic, double mu, double lo, double hi,
@@ -297,11 +378,9 @@ __global__ void verify_finish_kernel(int64_t M, bool is_int, int statistic, doub
   __shared__ unsigned long long s_k[32];
   __shared__ int s_batch_flag;
   if (!is_int && statistic == GG_BATCH_MEAN) {
-    if (threadIdx.x == 0) {
-      // dm = float(d.mean()) = pairwise_sum(d) / n               (guard.py:199-201)
-      const double dm = __ddiv_rn(np_pairwise_sum(static_cast<const double*>(d), M), static_cast<double>(M));
-      s_batch_flag = ((lo <= dm) && (dm <= hi)) ? 0 : 1;
-    }
+    // dm = float(d.mean()) = pairwise_sum(d) / n               (guard.py:199-201)
+    const double dm = __ddiv_rn(np_pairwise_sum_block(static_cast<const double*>(d), M), static_cast<double>(M));
+    if (threadIdx.x == 0) s_batch_flag = ((lo <= dm) && (dm <= hi)) ? 0 : 1;
     __syncthreads();
     for (int64_t i = threadIdx.x; i < M; i += blockDim.x) flags[i] = static_cast<uint8_t>(s_batch_flag);
   }
@@ -464,6 +543,52 @@ __global__ void digits_i64_kernel(const long long* w, int64_t K, int64_t Kp, int
   out[i] = make_int4(static_cast<int>(plane[0]), static_cast<int>(plane[1]), static_cast<int>(plane[2]), 0);
 }
 
+// fp32 -> tf32 (10-bit mantissa) rounded to nearest even; non-finite values pass through.
+__device__ __forceinline__ float tf32_rne(float x) {
+  const uint32_t u = __float_as_uint(x);
+  if ((u & 0x7f800000u) == 0x7f800000u) return x;
+  const uint32_t r = (u + 0xfffu + ((u >> 13) & 1u)) & 0xffffe000u;
+  // rounding up past the largest finite tf32 would give inf: truncate instead
+  return ((r & 0x7f800000u) == 0x7f800000u) ? __uint_as_float(u & 0xffffe000u) : __uint_as_float(r);
+}
+
+// 3xTF32 expansion of an fp32 operand [rows, K] into [rows, 3 * Ks]:
+// role 0 (A / X): [hi | hi | lo], role 1 (B / W): [hi | lo | hi]; hi = tf32(x),
+// lo = x - hi (exact in fp32).  A non-finite x is placed whole in the first
+// segment with zeros in the other two, so no inf * 0 term appears on either side.
+__global__ void split_tf32x3_kernel(const float* __restrict__ src, int64_t rows, int64_t K, int64_t ld, int role,
+                                    float* __restrict__ dst, int64_t ldd, int64_t Ks) {
+  const int64_t r = blockIdx.y;
+  const float* s = src + r * ld;
+  float* d = dst + r * ldd;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < Ks;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float h = 0.f, l = 0.f, x = 0.f;
+    if (k < K) {
+      x = s[k];
+      if (isfinite(x)) {
+        h = tf32_rne(x);
+        l = x - h;
+      } else {
+        h = x;
+      }
+    }
+    const bool fin = isfinite(x);
+    d[k] = h;
+    d[Ks + k] = fin ? (role == 0 ? h : l) : 0.f;
+    d[2 * Ks + k] = fin ? (role == 0 ? l : h) : 0.f;
+  }
+}
+
+// checksum side path of a 3xTF32 launch: [w | 0 | w] over the three K segments of
+// the expanded X (x = hi + lo enters the predicted sum exactly once)
+__global__ void f32x3_of_f64_kernel(const double* w, int64_t K, int64_t Ks, int64_t total, float* out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= total) return;
+  const int64_t seg = i / Ks, k = i - seg * Ks;
+  out[i] = (seg != 1 && seg < 3 && k < K) ? __double2float_rn(w[k]) : 0.f;
+}
+
 inline unsigned grid1(int64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
 }  // namespace
@@ -576,10 +701,32 @@ int launch_gemm_exact(int dtype, int accum, const void* X, int64_t M, int64_t K,
   return check_launch("gemm_exact");
 }
 
+int64_t tf32x3_segment(int64_t K) { return (K + 31) / 32 * 32; }
+
+int launch_split_tf32x3(const float* src, int64_t rows, int64_t K, int64_t ld, int role, float* dst, int64_t ldd,
+                        cudaStream_t s) {
+  if (rows < 1 || K < 1) return fail(GG_EINVAL, "split_tf32x3: empty operand");
+  if (role != 0 && role != 1) return fail(GG_EINVAL, "split_tf32x3: role must be 0 (A) or 1 (B)");
+  const int64_t Ks = tf32x3_segment(K);
+  if (ld < K || ldd < 3 * Ks) return fail(GG_EINVAL, "split_tf32x3: leading dims too small");
+  if (rows > 65535 * 1024) return fail(GG_EINVAL, "split_tf32x3: too many rows");
+  const int bs = 256;
+  const unsigned gx = static_cast<unsigned>(std::min<int64_t>((Ks + bs - 1) / bs, 64));
+  int64_t done = 0;
+  while (done < rows) {  // grid.y is limited to 65535 rows per launch
+    const int64_t n = std::min<int64_t>(rows - done, 65535);
+    split_tf32x3_kernel<<<dim3(gx, static_cast<unsigned>(n)), bs, 0, s>>>(src + done * ld, n, K, ld, role,
+                                                                        dst + done * ldd, ldd, Ks);
+    done += n;
+  }
+  return check_launch("split_tf32x3");
+}
+
 size_t checksum_aux_bytes(int ab_kind, int64_t K) {
   if (K < 1) return 0;
   const int64_t Kp = aux_padded(K);
   switch (ab_kind) {
+    case GG_TF32X3: return static_cast<size_t>(aux_padded(3 * tf32x3_segment(K))) * 4;
     case GG_BF16: case GG_F16: case GG_F32: return static_cast<size_t>(Kp) * 4;
     case GG_I8: return static_cast<size_t>(Kp / 4) * 16;
     default: return 0;
@@ -590,6 +737,12 @@ int launch_checksum_aux(int ab_kind, const void* w_sum, int64_t K, void* aux, cu
   if (K < 1) return fail(GG_EINVAL, "checksum_aux: empty w_sum");
   const int64_t Kp = aux_padded(K);
   switch (ab_kind) {
+    case GG_TF32X3: {
+      const int64_t Ks = tf32x3_segment(K), total = aux_padded(3 * Ks);
+      f32x3_of_f64_kernel<<<grid1(total, 256), 256, 0, s>>>(static_cast<const double*>(w_sum), K, Ks, total,
+                                                             static_cast<float*>(aux));
+      break;
+    }
     case GG_BF16: case GG_F16: case GG_F32:
       f32_of_f64_kernel<<<grid1(Kp, 256), 256, 0, s>>>(static_cast<const double*>(w_sum), K, Kp,
                                                        static_cast<float*>(aux));
@@ -602,6 +755,12 @@ int launch_checksum_aux(int ab_kind, const void* w_sum, int64_t K, void* aux, cu
       return fail(GG_EINVAL, "checksum_aux: unknown ab_kind");
   }
   return check_launch("checksum_aux");
+}
+
+int launch_batch_mean_finish(int64_t M, double mu, double lo, double hi, const double* d, uint8_t* flags,
+                             double* max_disc, int32_t* nflag, uint8_t* triggered, cudaStream_t s) {
+  verify_finish_kernel<<<1, 256, 0, s>>>(M, false, GG_BATCH_MEAN, mu, lo, hi, d, flags, max_disc, nflag, triggered);
+  return check_launch("batch_mean_finish");
 }
 
 int launch_reduce(int dtype, const void* A, int64_t rows, int64_t cols, int axis, void* out, cudaStream_t s) {

@@ -50,6 +50,11 @@ int gg_checksum_aux(int32_t ab_kind, const void* w_sum, int64_t K, void* aux_out
   return gg::launch_checksum_aux(ab_kind, w_sum, K, aux_out, static_cast<cudaStream_t>(stream));
 }
 
+int gg_split_tf32x3(const float* src, int64_t rows, int64_t K, int64_t ld, int32_t role, float* dst, int64_t ldd,
+                    void* stream) {
+  return gg::launch_split_tf32x3(src, rows, K, ld, role, dst, ldd, static_cast<cudaStream_t>(stream));
+}
+
 int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_t N, int64_t ldw, int32_t w_layout,
                         const void* bias, int32_t bias_dtype, int32_t chk_prec, void* w_sum_out,
                         void* bias_sum_out, void* stream) {

@@ -116,10 +116,11 @@ struct BandRows {
   unsigned long long key;
 };
 
+// Flags follow the per-sample rule; a batch_mean launch has its flags re-derived from
+// every d by the launcher's follow-up pass (NumPy's pairwise mean, guard.py:198-201).
 template <bool INT>
 __device__ __forceinline__ BandRows<INT> band_rows(const Params& p, int mb, int lane, const unsigned long long (&obs)[4],
                                                   const unsigned long long (&pred)[4]) {
-  const bool per_sample = INT || p.statistic == GG_PER_SAMPLE;
   BandRows<INT> r;
   r.nflag = 0;
   r.key = 0;
@@ -153,7 +154,7 @@ __device__ __forceinline__ BandRows<INT> band_rows(const Params& p, int mb, int 
       const unsigned long long k = f64_bits_nan(gb) ? 0ull : gb + 1ull;  // gap_key
       r.key = k > r.key ? k : r.key;
     }
-    if (per_sample) r.nflag += r.flag[q] ? 1 : 0;
+    r.nflag += r.flag[q] ? 1 : 0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -167,13 +168,12 @@ __device__ __forceinline__ BandRows<INT> band_rows(const Params& p, int mb, int 
 // Row stores (d, per-sample flags) and the band summary of band_rows' result.
 template <bool INT>
 __device__ __forceinline__ void store_band(const Params& p, int mb, int lane, const BandRows<INT>& r) {
-  const bool per_sample = INT || p.statistic == GG_PER_SAMPLE;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int row = mb * BM + lane + 32 * q;
     if (row >= p.M) continue;
     static_cast<unsigned long long*>(p.d)[row] = r.dbits[q];
-    if (per_sample) p.flags[row] = r.flag[q] ? 1 : 0;
+    p.flags[row] = r.flag[q] ? 1 : 0;
   }
   if (lane == 0) {
     p.ws.band_nflag[mb] = r.nflag;
@@ -181,19 +181,9 @@ __device__ __forceinline__ void store_band(const Params& p, int mb, int lane, co
   }
 }
 
-// The launch summary from the totals (and the batch-mean flags, which need every d).
+// The launch summary from the totals.
 template <bool INT>
 __device__ void publish_summary(const Params& p, int lane, int nf, unsigned long long mk) {
-  if (!INT && p.statistic == GG_BATCH_MEAN) {
-    double s = 0.0;  // fixed lane -> row assignment and shuffle tree: deterministic
-    for (int r = lane; r < p.M; r += 32) s += ldcg_f64(&static_cast<double*>(p.d)[r]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const double dm = s / static_cast<double>(p.M);
-    const bool inside = (p.lo <= dm) && (dm <= p.hi);
-    for (int r = lane; r < p.M; r += 32) p.flags[r] = inside ? 0 : 1;
-    nf = inside ? 0 : p.M;
-  }
   if (lane == 0) {
     *p.nflag = nf;
     *p.triggered = nf > 0 ? 1 : 0;
@@ -210,7 +200,6 @@ __device__ void finish_band(const Params& p, int mb, int lane, const unsigned lo
 #ifdef GG_TRACE
   const long long fb_t0 = clock64();
 #endif
-  const bool bmean = !INT && p.statistic == GG_BATCH_MEAN;
   const BandRows<INT> r = band_rows<INT>(p, mb, lane, obs, pred);
 #ifdef GG_TRACE
   const long long fb_t1 = clock64();
@@ -218,11 +207,7 @@ __device__ void finish_band(const Params& p, int mb, int lane, const unsigned lo
   // Launch summary: atomicMax of the band's gap key, then a release-add of
   // {1 << 32 | flagged rows}; the band that completes the count acquires and reads the
   // totals.  The release has no outstanding stores to wait for when the rows are stored
-  // after it (the batch-mean statistic reads every row's d, so there they go first).
-  if (bmean) {
-    store_band<INT>(p, mb, lane, r);
-    __syncwarp();
-  }
+  // after it.
   int last = 0;
   unsigned long long fin_rows = 0, fin_key = 0;
   if (lane == 0 && !GG_DBG(8192)) {
@@ -240,7 +225,7 @@ __device__ void finish_band(const Params& p, int mb, int lane, const unsigned lo
 #ifdef GG_TRACE
   const long long fb_t2 = clock64();
 #endif
-  if (!bmean) store_band<INT>(p, mb, lane, r);
+  store_band<INT>(p, mb, lane, r);
 #ifdef GG_TRACE
   if (lane == 0 && g_trace != nullptr) {
     const size_t b = static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV;

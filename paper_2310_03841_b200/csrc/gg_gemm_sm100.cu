@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -182,16 +183,61 @@ __global__ void replay_prepare_kernel(const uint8_t* rows, int M, int m_tiles, u
   }
 }
 
+// Per device, once per instantiation: the shared-memory opt-in is a per-device
+// function attribute (a process driving several GPUs configures each one).
+template <int KIND, int OUT, bool PROTECT, bool CLAIM>
+int configure_instance(int dev) {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return 0;
+  auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT, CLAIM>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES) != cudaSuccess)
+    return fail(GG_ECUDA, "cudaFuncSetAttribute(max dynamic smem, pair kernel) failed");
+  done[dev] = true;
+  return 0;
+}
+
+int current_device(int& dev) {
+  dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(GG_EUNSUPPORTED, "protected_gemm: device ordinal beyond 63");
+  return 0;
+}
+
+// CTA pairs that can be resident at once on this device (every instantiation has the
+// same shared memory and block size).  The grid never exceeds it: the claimed split-band
+// folds (CLAIM) spin on bands owned by other pairs, so a pair that could not be
+// scheduled (MPS limits, green contexts, kernels on other streams) would hang the launch.
+int max_coresident_pairs(int dev) {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache[dev]) return cache[dev];
+  auto kern = pair::gg_protected_gemm_pair_kernel<K_BF16, O_BF16, true, false>;
+  int n = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES) == cudaSuccess) {
+    cudaLaunchConfig_t occ{};
+    occ.gridDim = dim3(2);
+    occ.blockDim = dim3(pair::THREADS);
+    occ.dynamicSmemBytes = pair::SMEM_BYTES;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &occ) != cudaSuccess) n = 0;
+  }
+  cudaGetLastError();
+  if (n < 1) n = num_sms() / 2;
+  cache[dev] = n;
+  return n;
+}
+
 template <int KIND, int OUT, bool PROTECT, bool CLAIM = false>
 int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p, int grid,
                          cudaStream_t s) {
   auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT, CLAIM>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES) != cudaSuccess)
-      return fail(GG_ECUDA, "cudaFuncSetAttribute(max dynamic smem, pair kernel) failed");
-    configured = true;
-  }
+  int dev;
+  int rc = current_device(dev);
+  if (rc) return rc;
+  rc = configure_instance<KIND, OUT, PROTECT, CLAIM>(dev);
+  if (rc) return rc;
 #ifdef GG_NO_PDL
   kern<<<grid, pair::THREADS, pair::SMEM_BYTES, s>>>(ta, tb, tc, p);
 #else
@@ -330,7 +376,10 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.mu_zero = d->mu == 0.0 ? 1 : 0;
   p.lo_key = std::isnan(d->lo) ? ~0ull : f64_order_key(f64_bits_host(d->lo));  // NaN bounds: every row flags
   p.hi_key = std::isnan(d->hi) ? 0ull : f64_order_key(f64_bits_host(d->hi));
-  p.statistic = d->statistic;
+  // the kernel applies the per-sample rule; batch_mean flags need every d and are
+  // re-derived below by one pairwise-mean pass (guard.py:198-201)
+  const bool batch_mean = !int_kind && protect && d->statistic == GG_BATCH_MEAN;
+  p.statistic = GG_PER_SAMPLE;
   p.d = d->d;
   p.flags = d->flags;
   p.max_disc = d->max_disc;
@@ -361,8 +410,11 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
     rc = check_launch("replay_prepare");
     if (rc) return rc;
   }
+  int dev;
+  rc = current_device(dev);
+  if (rc) return rc;
   const int pair_tiles = ((p.M + 2 * pair::BM - 1) / (2 * pair::BM)) * p.n_tiles;
-  const int pairs = pair_tiles < num_sms() / 2 ? pair_tiles : num_sms() / 2;
+  const int pairs = std::min(pair_tiles, std::min(num_sms() / 2, max_coresident_pairs(dev)));
   const int grid = 2 * pairs;
   // A bands streamed concurrently by all pairs (256 rows x K each): keep them L2-resident
   const double a_footprint = static_cast<double>(pairs) * 2 * pair::BM * static_cast<double>(d->K) * elem;
@@ -378,16 +430,23 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
 
   switch (kind) {
     case K_BF16:
-      return out == O_BF16 ? dispatch_protect<K_BF16, O_BF16>(protect, ta, tb, tc, p, grid, s)
-                           : dispatch_protect<K_BF16, O_F32>(protect, ta, tb, tc, p, grid, s);
+      rc = out == O_BF16 ? dispatch_protect<K_BF16, O_BF16>(protect, ta, tb, tc, p, grid, s)
+                         : dispatch_protect<K_BF16, O_F32>(protect, ta, tb, tc, p, grid, s);
+      break;
     case K_F16:
-      return out == O_F16 ? dispatch_protect<K_F16, O_F16>(protect, ta, tb, tc, p, grid, s)
-                          : dispatch_protect<K_F16, O_F32>(protect, ta, tb, tc, p, grid, s);
+      rc = out == O_F16 ? dispatch_protect<K_F16, O_F16>(protect, ta, tb, tc, p, grid, s)
+                        : dispatch_protect<K_F16, O_F32>(protect, ta, tb, tc, p, grid, s);
+      break;
     case K_TF32:
-      return dispatch_protect<K_TF32, O_F32>(protect, ta, tb, tc, p, grid, s);
+      rc = dispatch_protect<K_TF32, O_F32>(protect, ta, tb, tc, p, grid, s);
+      break;
     default:
-      return dispatch_protect<K_I8, O_I32>(protect, ta, tb, tc, p, grid, s);
+      rc = dispatch_protect<K_I8, O_I32>(protect, ta, tb, tc, p, grid, s);
   }
+  if (rc == 0 && batch_mean)
+    rc = launch_batch_mean_finish(d->M, d->mu, d->lo, d->hi, static_cast<const double*>(d->d), d->flags, d->max_disc,
+                                  d->nflag, d->triggered, s);
+  return rc;
 }
 
 #ifdef GG_TRACE

@@ -45,9 +45,14 @@ int launch_flip_bits(void* ptr, int elem_bytes, const int64_t* elem_idx, const i
 int launch_gemm_exact(int dtype, int accum, const void* X, int64_t M, int64_t K, const void* Wt, int64_t N,
                       const void* bias, void* Y, cudaStream_t s);
 int launch_reduce(int dtype, const void* A, int64_t rows, int64_t cols, int axis, void* out, cudaStream_t s);
+// batch_mean statistic of a protected launch: flags / summaries from every d (pairwise mean)
+int launch_batch_mean_finish(int64_t M, double mu, double lo, double hi, const double* d, uint8_t* flags,
+                             double* max_disc, int32_t* nflag, uint8_t* triggered, cudaStream_t s);
 int launch_round(int dtype, const double* in, void* out, int64_t n, cudaStream_t s);
 
 size_t checksum_aux_bytes(int ab_kind, int64_t K);
+int launch_split_tf32x3(const float* src, int64_t rows, int64_t K, int64_t ld, int role, float* dst, int64_t ldd,
+                        cudaStream_t s);
 int launch_checksum_aux(int ab_kind, const void* w_sum, int64_t K, void* aux, cudaStream_t s);
 
 // implemented in gg_calib.cu

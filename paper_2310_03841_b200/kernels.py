@@ -189,12 +189,46 @@ def build_desc(
     return d
 
 
-def checksum_aux(w_sum: torch.Tensor, ab_dtype: torch.dtype) -> torch.Tensor | None:
+F32_MODES = ("3xtf32", "tf32")
+
+
+def _f32_mode(mode: str) -> str:
+    if mode not in F32_MODES:
+        raise ValueError(f"f32_mode must be one of {F32_MODES}, got {mode!r}")
+    return mode
+
+
+def tf32x3_segment(K: int) -> int:
+    """Width of one K segment of a 3xTF32 expansion (K rounded up to 32)."""
+    return (K + 31) // 32 * 32
+
+
+def split_tf32x3(t: torch.Tensor, role: int) -> torch.Tensor:
+    """gg_split_tf32x3: fp32 [rows, K] -> [rows, 3*Ks]; role 0 (X): [hi|hi|lo],
+    role 1 (W [N, K]): [hi|lo|hi].  A tf32 launch over the expanded operands
+    computes the binary32 GEMM to ~2^-21 per product (3xTF32)."""
+    dev = _require_cuda(t)
+    if t.dtype != torch.float32 or t.dim() != 2:
+        raise ValueError("split_tf32x3 takes a 2-D float32 tensor")
+    if t.stride(1) != 1:
+        t = t.contiguous()
+    rows, K = t.shape
+    Ks = tf32x3_segment(K)
+    out = torch.empty((rows, 3 * Ks), dtype=torch.float32, device=dev)
+    L.check(L.load().gg_split_tf32x3(t.data_ptr(), rows, K, t.stride(0), int(role), out.data_ptr(), out.stride(0),
+                                     _stream(dev)), "gg_split_tf32x3")
+    return out
+
+
+def checksum_aux(w_sum: torch.Tensor, ab_dtype: torch.dtype, f32_mode: str = "3xtf32") -> torch.Tensor | None:
     """Side-path encoding of w_sum for the fused checksum (gg_checksum_aux):
-    fp32(w_sum) for float operands (bf16 / fp16 / tf32), signed base-256 digit
-    planes for int8.  Computed once per weight."""
+    fp32(w_sum) for float operands (bf16 / fp16 / tf32; [w | 0 | w] over the
+    three segments of a 3xTF32 launch), signed base-256 digit planes for int8.
+    Computed once per weight."""
     dev = _require_cuda(w_sum)
     kind = TORCH_TO_GG[ab_dtype]
+    if ab_dtype == torch.float32 and _f32_mode(f32_mode) == "3xtf32":
+        kind = L.GG_TF32X3
     K = w_sum.numel()
     nbytes = int(L.load().gg_checksum_aux_bytes(kind, K))
     if nbytes == 0:
@@ -225,6 +259,27 @@ def default_out_dtype(ab: torch.dtype) -> torch.dtype:
             torch.int8: torch.int32}[ab]
 
 
+def _prepare_operands(x, w, w_sum, w_aux, protect, f32_mode, w_split):
+    """TMA-ready operands (16-byte pitches) and the matching checksum encoding;
+    fp32 operands are expanded for 3xTF32 unless f32_mode="tf32"."""
+    if x.dtype == torch.float32 and _f32_mode(f32_mode) == "3xtf32":
+        xs = split_tf32x3(x, 0)
+        ws = w_split if w_split is not None else split_tf32x3(w, 1)
+        if ws.shape != (w.shape[0], xs.shape[1]):
+            raise ValueError("w_split does not match the weight's 3xTF32 expansion")
+        if protect and w_aux is None and w_sum is not None:
+            w_aux = checksum_aux(w_sum, torch.float32, "3xtf32")
+    else:
+        xs, ws = _pad_k(x), _pad_k(w)
+        if protect and w_aux is None and w_sum is not None:
+            w_aux = checksum_aux(w_sum, x.dtype, f32_mode)
+    if protect and w_aux is not None:
+        need = int(L.load().gg_checksum_aux_bytes(TORCH_TO_GG[xs.dtype], xs.shape[1]))
+        if w_aux.numel() * w_aux.element_size() < need:
+            raise ValueError("w_aux does not match this launch's operand kind (3xTF32 vs tf32?)")
+    return xs, ws, w_aux
+
+
 def protected_gemm(
     x: torch.Tensor,
     w: torch.Tensor,
@@ -243,24 +298,25 @@ def protected_gemm(
     out: torch.Tensor | None = None,
     result: CheckResult | None = None,
     ws_key=None,
+    f32_mode: str = "3xtf32",
+    w_split: torch.Tensor | None = None,
 ) -> tuple[torch.Tensor, CheckResult | None]:
     """K1: y = x @ w.T + bias with the fused checksum check (one launch).
 
     x [M, K], w [N, K] (torch Linear layout), bias [N] (f32, or i32 for int8).
+    fp32 operands run as 3xTF32 (binary32 accuracy; `w_split` may hold the
+    weight's cached `split_tf32x3(w, 1)`) unless f32_mode="tf32" (one tf32 pass).
     Returns (y, CheckResult or None when protect=False).
     """
     dev = _require_cuda(x, w, bias)
     _check_gemm_operands(x, w, bias)
-    x = _pad_k(x)
-    w = _pad_k(w)
+    x, w, w_aux = _prepare_operands(x, w, w_sum, w_aux, protect, f32_mode, w_split)
     M, N = x.shape[0], w.shape[0]
     odt = out_dtype or default_out_dtype(x.dtype)
     y = out if out is not None else torch.empty((M, N), dtype=odt, device=dev)
     if protect:
         if w_sum is None:
             raise ValueError("protect=True needs the offline checksum w_sum")
-        if w_aux is None:
-            w_aux = checksum_aux(w_sum, x.dtype)
         result = result or CheckResult.empty(M, x.dtype == torch.int8, dev)
         ws = workspace(M, N, dev, ws_key)
     else:
@@ -289,6 +345,7 @@ def packed_output_campaign(
     mu: float = 0.0,
     lo: float = 0.0,
     hi: float = 0.0,
+    f32_mode: str = "3xtf32",
 ) -> tuple[torch.Tensor, int]:
     """Campaign engine for independent single-fault trials on one layer input:
     fault i is detected iff its row is flagged by a launch that injects it.
@@ -316,7 +373,7 @@ def packed_output_campaign(
     for g in groups:
         inj = injections_to_device([faults[i] for i in g], dev)
         protected_gemm(x, w, bias, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi, injections=inj,
-                       out=y, result=res)
+                       out=y, result=res, f32_mode=f32_mode)
         idx = torch.tensor(g, dtype=torch.int64, device=dev)
         rows = torch.tensor([faults[i].row for i in g], dtype=torch.int64, device=dev)
         detected[idx] = res.flags[rows].bool()
@@ -340,21 +397,21 @@ def replay_tiles(
     statistic: int = L.GG_PER_SAMPLE,
     changed: torch.Tensor | None = None,
     ws_key=None,
+    f32_mode: str = "3xtf32",
+    w_split: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """K4: recompute only the M-bands holding a flagged row, in place in y.
 
+    Must use the same operands, f32_mode and ws_key as the launch it replays.
     Returns the device scalar count of outputs whose bytes changed (0 means
     the recompute reproduced the flagged output: guard.py:590-594).
     """
     dev = _require_cuda(x, w, y, replay_rows)
     _check_gemm_operands(x, w, bias)
-    x = _pad_k(x)
-    w = _pad_k(w)
+    x, w, w_aux = _prepare_operands(x, w, w_sum, w_aux, True, f32_mode, w_split)
     M, N = x.shape[0], w.shape[0]
     changed = changed if changed is not None else torch.zeros(1, dtype=torch.int32, device=dev)
     ws = workspace(M, N, dev, ws_key)
-    if w_aux is None:
-        w_aux = checksum_aux(w_sum, x.dtype)
     desc = build_desc(x, w, y, bias, protect=True, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
                       statistic=statistic, result=result, ws=ws, replay_rows=replay_rows, changed=changed)
     L.check(L.load().gg_replay_tiles(ctypes.byref(desc), _stream(dev)), "gg_replay_tiles")

@@ -6,10 +6,14 @@ fields) keep the reference's names, storage conventions, validation and error
 messages.  The arithmetic runs on the B200:
 
 * `gemm` launches the tcgen05 GEMM of libgemmguard_b200.so (engine
-  ``"tensor"``: kind::i8 for int8, kind::f16 for binary16-emulated,
-  kind::tf32 for binary32) or the reference-order CUDA-core fold (engine
-  ``"exact"``, bit-identical to numerics.py:222-289 for every dtype/accum
-  pair, and the only engine for binary64 and int32 operands);
+  ``"tensor"``: kind::i8 for int8, kind::f16 for binary16-emulated, and
+  3xTF32 on kind::tf32 for binary32 — x*w = hi*hi + hi*lo + lo*hi, binary32
+  accuracy to ~2^-21 per product) or the reference-order CUDA-core fold
+  (engine ``"exact"``, bit-identical to numerics.py:222-289 for every
+  dtype/accum pair, and the only engine for binary64 and int32 operands).
+  Engine ``"tf32"`` is the explicit opt-in for single-pass TF32 on binary32
+  operands (10-bit mantissa products: about 2^-11 relative error, far outside
+  the reference's binary32 arithmetic; other dtypes run as ``"tensor"``);
 * `reduce_rows` / `reduce_cols` are ascending device folds (numerics.py:292-305).
 
 `flip_bit` and `round_to` are scalar encodings helpers of the API
@@ -63,7 +67,7 @@ FLOAT_DTYPES = frozenset(_FIELDS)
 INT_DTYPES = frozenset(("int8", "int32"))
 DTYPE_TAGS = tuple(_ENC)
 
-ENGINES = ("tensor", "exact")
+ENGINES = ("tensor", "exact", "tf32")
 
 
 def default_engine() -> str:
@@ -237,7 +241,7 @@ def _check_gemm_args(X: Matrix2D, Wt: Matrix2D, bias, accum):
 
 def tensor_engine_applies(dtype: str, accum: Precision) -> bool:
     """The tcgen05 path covers int8 (int32 accumulate) and binary16/binary32
-    operands with binary32 accumulation (tf32 for binary32)."""
+    operands with binary32 accumulation (3xTF32, or opt-in tf32, for binary32)."""
     if dtype == "int8":
         return True
     return dtype in ("binary16-emulated", "binary32") and accum is Precision.BINARY32
@@ -247,9 +251,20 @@ def resolve_engine(dtype: str, accum: Precision, engine: str | None) -> str:
     e = engine or default_engine()
     if e not in ENGINES:
         raise ValueError(f"engine must be one of {ENGINES}, got {e!r}")
-    if e == "tensor" and not tensor_engine_applies(dtype, accum):
+    if e in ("tensor", "tf32") and not tensor_engine_applies(dtype, accum):
         return "exact"
+    if e == "tf32" and dtype != "binary32":
+        return "tensor"
     return e
+
+
+def f32_mode_of(engine: str) -> str:
+    """kernels.protected_gemm f32_mode of a tensor-path engine."""
+    return "tf32" if engine == "tf32" else "3xtf32"
+
+
+def is_tensor_engine(engine: str) -> bool:
+    return engine in ("tensor", "tf32")
 
 
 def device_bias(bias, dtype: str, engine: str) -> torch.Tensor | None:
@@ -261,7 +276,7 @@ def device_bias(bias, dtype: str, engine: str) -> torch.Tensor | None:
     if dtype in INT_DTYPES:
         with np.errstate(over="ignore"):
             return torch.from_numpy(b.astype(np.int32)).to(dev)  # bias.astype(int32), numerics.py:271
-    if engine == "tensor":
+    if is_tensor_engine(engine):
         with np.errstate(over="ignore"):
             return torch.from_numpy(b.astype(np.float32)).to(dev)  # bias.astype(acc = fp32)
     return torch.from_numpy(b.astype(np.float64)).to(dev)
@@ -270,8 +285,8 @@ def device_bias(bias, dtype: str, engine: str) -> torch.Tensor | None:
 def gemm_device(x: torch.Tensor, wt_nk: torch.Tensor | None, wt_kn: torch.Tensor | None, bias_dev,
                 dtype: str, accum: Precision, engine: str) -> torch.Tensor:
     """Device GEMM on prepared operands: x [M,K]; weight as [N,K] (tensor) or [K,N] (exact)."""
-    if engine == "tensor":
-        y, _ = K.protected_gemm(x, wt_nk, bias_dev, protect=False)
+    if is_tensor_engine(engine):
+        y, _ = K.protected_gemm(x, wt_nk, bias_dev, protect=False, f32_mode=f32_mode_of(engine))
         return y
     if dtype in INT_DTYPES:
         return K.gemm_exact(x, wt_kn, bias_dev, L.GG_P_I64)
@@ -291,7 +306,9 @@ def gemm(
     Same validation, defaults, rounding to the operand dtype and int32
     result for integer operands as the reference.  engine="exact" reproduces
     the reference's bits; engine="tensor" (default) runs tcgen05 and matches
-    bit-exactly for int8 and within the fp32-accumulation bound for floats.
+    bit-exactly for int8 and within the binary32-accumulation bound for floats
+    (binary32 operands as 3xTF32); engine="tf32" opts binary32 into one tf32
+    pass (about 2^-11 relative error per product).
     """
     bias, accum = _check_gemm_args(X, Wt, bias, accum)
     dtype = X.dtype
@@ -299,7 +316,7 @@ def gemm(
     x = X.to_device()
     wt = Wt.to_device()
     b = device_bias(bias, dtype, eng)
-    if eng == "tensor":
+    if is_tensor_engine(eng):
         y = gemm_device(x, wt.t().contiguous(), None, b, dtype, accum, eng)
     else:
         y = gemm_device(x, None, wt, b, dtype, accum, eng)

@@ -22,6 +22,7 @@ output is folded into a ``calib.RunningRange``, which is the device
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -43,7 +44,7 @@ class BatchForward:
     flagged: dict[int, np.ndarray] | None  # protect=True: layer -> [B] bool (any flagged row of the sample)
 
 
-_CHK: dict[int, tuple[torch.Tensor, int]] = {}
+_CHK: dict[int, tuple[torch.Tensor, int]] = {}  # id(weight Matrix2D) -> (w_sum, bias_sum), dropped with the weight
 
 
 def _checksum(layer, w_nk: torch.Tensor, bias: torch.Tensor):
@@ -53,6 +54,8 @@ def _checksum(layer, w_nk: torch.Tensor, bias: torch.Tensor):
         ws, bs = K.offline_checksum(w_nk, bias, L.GG_P_I64)
         got = (ws, int(bs.item()))
         _CHK[key] = got
+        # a reused id must never find a dead weight's checksum (model._DEV does the same)
+        weakref.finalize(layer.weight, _CHK.pop, key, None)
     return got
 
 

@@ -133,3 +133,19 @@ def test_product_path_fails_loudly_without_cuda():
 
     with pytest.raises(GemmGuardLibraryError, match="CUDA"):
         gemm(Matrix2D([[1.0]]), Matrix2D([[1.0]]))
+
+
+def test_checked_output_verdict_is_dropped_when_bytes_change():
+    """a fused verdict must not survive an in-place edit of the
+    output (a monkeypatched run_layer writing y[r, c] = bad, or a write through
+    a reshape view as guard.py:517-521 does)."""
+    from paper_2310_03841_b200.model import CheckedOutput
+
+    y = np.arange(12, dtype=np.float64).reshape(3, 4).view(CheckedOutput).bind(("chk", "eps", "outcome"))
+    assert y.fused_verdict() == ("chk", "eps", "outcome")
+    y[1, 2] = 99.0
+    assert y.fused_verdict() is None
+    z = np.arange(12, dtype=np.int32).reshape(3, 4).view(CheckedOutput).bind(("c", "e", "o"))
+    z.reshape(-1)[5] ^= 1 << 20  # write through a view
+    assert z.fused_verdict() is None
+    assert np.asarray(z).view(CheckedOutput).fused_verdict() is None  # derived arrays carry nothing

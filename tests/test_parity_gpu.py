@@ -7,7 +7,7 @@ reference-order verification, for flips and for everything computed by the
 "exact" engine; floating-point tensor-core GEMMs within the fp32-accumulation
 bound stated in `_fp_tolerance` (fp16/bf16 operands are exact in fp32, so the
 only error is the accumulation order: |dy| <= K * 2^-23 * sum|x w| + 1 ulp of
-the output; tf32 adds the operand truncation 2 * 2^-11 * sum|x w|)."""
+the output; binary32 operands run as 3xTF32 and add <= 2^-20 * sum|x w|)."""
 
 import math
 
@@ -34,7 +34,7 @@ def _fp_tolerance(x, wt, bias, y_ref, dtype):
     mag = np.abs(x.astype(np.float64)) @ np.abs(wt.astype(np.float64)) + np.abs(bias)
     K = x.shape[1]
     ulp = {"binary16-emulated": 2.0**-10, "binary32": 2.0**-23}[dtype]
-    tf32 = 2 * 2.0**-11 if dtype == "binary32" else 0.0
+    tf32 = 2.0**-20 if dtype == "binary32" else 0.0  # 3xTF32: lo*lo dropped, lo tf32-truncated
     return mag * (K * 2.0**-23 + tf32) + np.abs(y_ref) * ulp + 1e-30
 
 
@@ -118,46 +118,80 @@ def test_cfg1_fp32_1024_exact_engine_bit_identical_with_1000_flips():
         assert int(out.triggered) == trig and out.flagged == flagged
 
 
-def test_cfg1_tensor_engine_fused_check_detects_what_the_reference_detects_beyond_the_band():
-    """tf32 tensor path + fused checksum: flips whose reference |d| clears the
-    threshold by more than the tf32 noise band are flagged identically."""
+def test_cfg1_tensor_engine_fused_flags_equal_the_reference_on_1000_flips():
+    """Config 1 on the default tensor path (binary32 as 3xTF32 + the fused
+    check) at the REFERENCE's thresholds: for each of the 1000 golden output
+    flips the flagged rows and `triggered` equal the reference's.  A row may
+    differ only where the reference's d for that trial lies within the band
+    the two GEMMs' numerics can move it (twice the clean |d_tensor - d_ref|
+    of that row, plus the difference of the two injected shifts); the count of
+    such rows is reported (expected 0).  The tensor path's own epsilon
+    half-width stays within 2x of the reference's (7.1e-5)."""
     import torch
 
     from paper_2310_03841_b200 import kernels as K
 
     c = doc("cfg1.json")
-    x, wt, bias = cfg1_inputs(c["n"], c["seed"])
+    n = c["n"]
+    x, wt, bias = cfg1_inputs(n, c["seed"])
+    X, Wt = Matrix2D(x, "binary32"), Matrix2D(wt, "binary32")
+    Yref = gemm(X, Wt, bias=bias, accum=Precision.BINARY32, engine="exact")
+    assert sha(Yref.data) == c["Y_sha256"]
+    L = Mo.LayerSpec(0, "L0", "embed", n, n, n, Wt, bias)
+    chk = G.offline_checksum(L, Precision.BINARY64)
+    d_ref = G._discrepancies(X.widened(), Yref.widened(), chk)
+    assert sha(d_ref) == c["d_sha256"]
+    mu, sigma, lo, hi = c["eps"]
     xd = torch.from_numpy(x).cuda()
     wd = torch.from_numpy(np.ascontiguousarray(wt.T)).cuda()
     bd = torch.from_numpy(bias.astype(np.float32)).cuda()
-    L = Mo.LayerSpec(0, "L0", "embed", c["n"], c["n"], c["n"], Matrix2D(wt, "binary32"), bias)
-    chk = G.offline_checksum(L, Precision.BINARY64)
-    # calibrate the tf32 noise on clean rows
-    y, res = K.protected_gemm(xd, wd, bd, w_sum=chk.w_sum_device(), bias_sum=chk.bias_sum, lo=-1e30, hi=1e30)
-    dcl = res.d.cpu().numpy()
-    lo, hi = O.threshold_from_confidence(float(dcl.mean()), float(dcl.std(ddof=1)), 0.9999)
-    assert not (dcl < lo).any() and not (dcl > hi).any() or True
-    band = 6.0 * float(dcl.std(ddof=1))
-    y_host = y.cpu().numpy()
-    ref_y = O.gemm(x, wt, bias, "binary32", "binary32")
-    assert np.all(np.abs(y_host - ref_y) <= _fp_tolerance(x, wt, bias, ref_y, "binary32"))
-    n_checked = 0
-    for e, bit, _, _, _ in c["flips"][:200]:
-        row, col = divmod(e, c["n"])
-        orig = float(y_host[row, col])
-        bad = float(I._flipped(orig, bit, "binary32"))
-        if not math.isfinite(bad):
-            continue
-        shift = abs(bad - orig)
-        inj = [K.Injection(row=row, col=col, bit=bit)]
-        _, r2 = K.protected_gemm(xd, wd, bd, w_sum=chk.w_sum_device(), bias_sum=chk.bias_sum, lo=lo, hi=hi,
-                                 injections=inj)
-        flags = r2.flags.cpu().numpy()
-        if shift > (hi - lo) + band:
-            assert flags[row] == 1
-            n_checked += 1
-        assert flags.sum() <= 1
-    assert n_checked > 20
+    w_split = K.split_tf32x3(wd, 1)
+    kw = dict(w_sum=chk.w_sum_device(), bias_sum=chk.bias_sum, mu=mu, lo=lo, hi=hi, w_split=w_split)
+    y_t, res = K.protected_gemm(xd, wd, bd, **kw)
+    y_t = y_t.cpu().numpy()
+    d_t = res.d.cpu().numpy()
+    # the GEMM itself: binary32 accuracy (3xTF32 drops lo*lo and tf32-truncates lo: <= 2^-21 per product)
+    ref_y = Yref.widened()
+    mag = np.abs(x.astype(np.float64)) @ np.abs(wt.astype(np.float64)) + np.abs(bias)
+    assert np.all(np.abs(y_t - ref_y) <= mag * (n * 2.0**-23 + 2.0**-20) + np.abs(ref_y) * 2.0**-23)
+    # epsilon of the tensor path on the same clean rows, against the reference's
+    sig_t = float(np.std(d_t, ddof=1))
+    assert sig_t <= 2.0 * sigma, (sig_t, sigma)
+    band = 2.0 * np.abs(d_t - d_ref) + 1e-12
+    excused = []
+    for k, (e, bit, trig, flagged, _) in enumerate(c["flips"]):
+        row, col = divmod(e, n)
+        _, r2 = K.protected_gemm(xd, wd, bd, injections=[K.Injection(row=row, col=col, bit=bit)], **kw)
+        got = set(np.flatnonzero(r2.flags.cpu().numpy()).tolist())
+        want = set(flagged)
+        for r in got ^ want:
+            if r == row:
+                o_ref, o_t = float(np.float32(ref_y[row, col])), float(np.float32(y_t[row, col]))
+                dl_ref = float(I._flipped(o_ref, bit, "binary32")) - o_ref
+                dl_t = float(I._flipped(o_t, bit, "binary32")) - o_t
+                dr, b = d_ref[r] - dl_ref, band[r] + 2.0 * abs(dl_t - dl_ref)
+            else:
+                dr, b = d_ref[r], band[r]
+            assert min(abs(dr - lo), abs(dr - hi)) <= b, (k, r, dr, lo, hi, b)
+            excused.append((k, r))
+        if not (got ^ want):
+            assert bool(r2.triggered.item()) == bool(trig)
+    print(f"cfg1 tensor path: sigma {sig_t:.3e} vs reference {sigma:.3e}; "
+          f"{len(excused)} flag differences inside the numerics band over 1000 flips")
+    assert len(excused) <= 5
+
+
+def test_cfg1_tf32_opt_in_engine_is_single_pass_tf32():
+    """Plain TF32 stays available as an explicit engine; it is narrower than
+    binary32 (about 2^-11 per product), which is why it is not the default."""
+    c = doc("cfg1.json")
+    x, wt, bias = cfg1_inputs(c["n"], c["seed"])
+    X, Wt = Matrix2D(x, "binary32"), Matrix2D(wt, "binary32")
+    y32 = gemm(X, Wt, bias=bias, accum=Precision.BINARY32, engine="tensor").widened()
+    y19 = gemm(X, Wt, bias=bias, accum=Precision.BINARY32, engine="tf32").widened()
+    ref = gemm(X, Wt, bias=bias, accum=Precision.BINARY32, engine="exact").widened()
+    e32, e19 = float(np.abs(y32 - ref).max()), float(np.abs(y19 - ref).max())
+    assert e19 > 30 * e32, (e19, e32)
 
 
 # ----------------------------------------------------- end-to-end toy pipelines
