@@ -169,7 +169,7 @@ GG_API int gg_offline_checksum(int32_t w_dtype, const void* W, int64_t K, int64_
  *                     so x*w is one fp32 FMA (|w - w_sum| <= 2^-24 |w_sum|),
  *                     folded by TwoSum into an fp32 (hi, lo) pair;
  *   GG_F32 (tf32):    float  [Kp] = fp32(w_sum) (as the 16-bit kinds);
- *   GG_TF32X3:        float [3*Ks, padded to 128] = [w | 0 | w] over the
+ *   GG_TF32X3:        float [3*Ks, padded to 128] = [0 | w | w] over the
  *                     three segments of a gg_split_tf32x3 expansion (K is the
  *                     original K; Ks = K rounded up to 32);
  *   GG_I8:            int32x4 [Kp/4] signed base-256 digit planes of the int64
@@ -181,15 +181,17 @@ GG_API int gg_checksum_aux(int32_t ab_kind, const void* w_sum, int64_t K, void* 
 /* binary32 at binary32 accuracy on the tf32 tensor pipe (3xTF32).  Expands an
  * fp32 operand [rows, K] (row pitch ld) into dst [rows, 3*Ks] (row pitch ldd >=
  * 3*Ks, Ks = K rounded up to 32; pads zero):
- *   role 0 (A = X): [hi | hi | lo]        role 1 (B = W [N, K]): [hi | lo | hi]
+ *   role 0 (A = X): [hi | lo | hi]        role 1 (B = W [N, K]): [lo | hi | hi]
  * with hi = x rounded to tf32 (RNE) and lo = x - hi (exact in fp32).  A
  * gg_protected_gemm launch with ab_kind GG_F32 over the expanded operands
- * (K' = 3*Ks) accumulates hi*hi + hi*lo + lo*hi per product in fp32 — the
+ * (K' = 3*Ks) accumulates hi*lo + lo*hi + hi*hi per product in fp32 — the
  * binary32 product of numerics.gemm (numerics.py:222-234) to ~2^-21 instead of
- * tf32's 2^-11 — and, with w_aux = gg_checksum_aux(GG_TF32X3, w_sum, K), its
- * predicted row sum is (hi + lo) . w = x . w exactly as before.  Non-finite x
- * are kept whole in the first segment (zeros elsewhere).  Plain single-pass
- * TF32 stays available as an explicit opt-in (ab_kind GG_F32 on x itself). */
+ * tf32's 2^-11, small cross terms first because the tensor core's fp32
+ * accumulator truncates each step by a fraction of its own magnitude — and,
+ * with w_aux = gg_checksum_aux(GG_TF32X3, w_sum, K), its predicted row sum is
+ * (lo + hi) . w = x . w exactly as before.  Non-finite x are kept whole in the
+ * last segment (zeros elsewhere).  Plain single-pass TF32 stays available as
+ * an explicit opt-in (ab_kind GG_F32 on x itself). */
 GG_API int gg_split_tf32x3(const float* src, int64_t rows, int64_t K, int64_t ld, int32_t role,
                            float* dst, int64_t ldd, void* stream);
 

@@ -204,9 +204,10 @@ def tf32x3_segment(K: int) -> int:
 
 
 def split_tf32x3(t: torch.Tensor, role: int) -> torch.Tensor:
-    """gg_split_tf32x3: fp32 [rows, K] -> [rows, 3*Ks]; role 0 (X): [hi|hi|lo],
-    role 1 (W [N, K]): [hi|lo|hi].  A tf32 launch over the expanded operands
-    computes the binary32 GEMM to ~2^-21 per product (3xTF32)."""
+    """gg_split_tf32x3: fp32 [rows, K] -> [rows, 3*Ks]; role 0 (X): [hi|lo|hi],
+    role 1 (W [N, K]): [lo|hi|hi].  A tf32 launch over the expanded operands
+    computes the binary32 GEMM to ~2^-21 per product (3xTF32), the small
+    cross terms accumulated first."""
     dev = _require_cuda(t)
     if t.dtype != torch.float32 or t.dim() != 2:
         raise ValueError("split_tf32x3 takes a 2-D float32 tensor")
