@@ -58,6 +58,11 @@ enum gg_precision {
 enum gg_statistic { GG_PER_SAMPLE = 0, GG_BATCH_MEAN = 1 };    /* guard.py:93  */
 enum gg_inj_target { GG_INJ_OUTPUT = 0, GG_INJ_ACCUMULATOR = 1 };
 enum gg_inj_mode { GG_INJ_BITFLIP = 0, GG_INJ_SET_VALUE = 1 }; /* injector.py:49-50 */
+/* Epilogue activation applied to each stored output AFTER its observed row sum:
+ * the check covers the raw (rounded, bias-included) GEMM output exactly as
+ * guard.py:10-11 / model.py:367-368, the activation of that value is what is
+ * stored (model.finish_layer_output's GELU, model.py:281-285, 318-319). */
+enum gg_epilogue_act { GG_ACT_NONE = 0, GG_ACT_GELU_TANH = 1 /* bf16 / fp16 outputs */ };
 
 enum gg_error {
   GG_OK = 0,
@@ -125,6 +130,8 @@ typedef struct gg_gemm_desc {
   /* replay (gg_replay_tiles only): */
   const uint8_t* replay_rows; /* [M] rows whose M-bands are recomputed       */
   int32_t* changed;           /* scalar: outputs whose bytes changed         */
+
+  int32_t epilogue_act;       /* gg_epilogue_act (0: store the GEMM output)   */
 } gg_gemm_desc;
 
 /* Library identity. */
@@ -260,6 +267,18 @@ GG_API int gg_minmax(int32_t dtype, const void* Y, int64_t M, int64_t N, int64_t
  * per sample, giving H [B*T, N/3].  NumPy integer semantics: bit-exact. */
 GG_API int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int64_t ldy,
                          int32_t relu, int32_t shift, int32_t qkv, int8_t* H, void* stream);
+
+/* Transformer glue of the protected ViT / Swin forward (not a reference
+ * function: the reference's toy pipeline glue is model.prepare_layer_input /
+ * finish_layer_output, model.py:288-331; attention and layer norm stay
+ * unprotected as in PAPER.md:221).  Residual update and layer norm in one
+ * pass: if y != NULL, h_out = round(h + y) (h_out may alias h); then
+ * ln_out = LN(h_out or h) * gamma + beta with fp32 statistics over rows of D
+ * (D a multiple of 32 x 16 bytes up to 8 such chunks per lane; dtype
+ * GG_BF16, GG_F16 or GG_F32; 16-byte aligned, contiguous rows). */
+GG_API int gg_add_layernorm(int32_t dtype, const void* h, const void* y, int64_t rows, int64_t D,
+                            const float* gamma, const float* beta, float eps, void* h_out,
+                            void* ln_out, void* stream);
 
 #ifdef __cplusplus
 }

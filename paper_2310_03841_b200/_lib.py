@@ -23,6 +23,7 @@ GG_P_F16, GG_P_F32, GG_P_F64, GG_P_I64 = range(4)
 GG_PER_SAMPLE, GG_BATCH_MEAN = 0, 1
 GG_INJ_OUTPUT, GG_INJ_ACCUMULATOR = 0, 1
 GG_INJ_BITFLIP, GG_INJ_SET_VALUE = 0, 1
+GG_ACT_NONE, GG_ACT_GELU_TANH = 0, 1
 GG_OK, GG_EINVAL, GG_ECUDA, GG_EWORKSPACE, GG_EUNSUPPORTED = 0, -1, -2, -3, -4
 
 # every symbol include/gemmguard_b200.h declares
@@ -44,6 +45,7 @@ EXPORTED_SYMBOLS = (
     "gg_running_stats",
     "gg_minmax",
     "gg_int_finish",
+    "gg_add_layernorm",
 )
 
 
@@ -93,6 +95,7 @@ class GGGemmDesc(ctypes.Structure):
         ("workspace_bytes", c_size_t),
         ("replay_rows", c_void_p),
         ("changed", c_void_p),
+        ("epilogue_act", c_int32),
     ]
 
 
@@ -158,6 +161,9 @@ def load(path: Path | None = None):
     lib.gg_int_finish.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32, c_void_p,
                                   c_void_p]
     lib.gg_round_f64_to.restype = c_int32
+    lib.gg_add_layernorm.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, ctypes.c_float,
+                                     c_void_p, c_void_p, c_void_p]
+    lib.gg_add_layernorm.restype = c_int32
     lib.gg_round_f64_to.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p]
     _lib = lib
     return lib

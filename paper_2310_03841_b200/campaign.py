@@ -1,0 +1,287 @@
+"""Batched, device-resident injection campaigns on a protected model.
+
+The reference runs one host-driven inference per injection: `injected_forward`
+re-runs the whole model from layer 0 on a scratch copy (injector.py:224-287),
+`run_campaign` stratifies n trials per layer with a per-trial RNG seeded by
+(seed, layer, k) (injector.py:451-565) and `evaluate_detection` counts a
+trial as a true positive when the output changed class AND the injected
+layer's check fired (guard.py:700-792).  On the B200 the same trial semantics
+run as a batch:
+
+* one trial per image of a batch: every image carries its own single output
+  fault in its own rows of the injected layer's launch (faults in distinct
+  rows never interact: the check is per row, guard.py:188-215, and images are
+  independent in a ViT), applied in the GEMM epilogue before the observed
+  sums (K1's in-epilogue injection; the reference corrupts the stored output
+  before the check, guard.py:515-523);
+* prefix reuse: the clean forward caches every protected layer's (residual,
+  input), and a trial batch restarts at its layer (`ProtectedViT.resume`);
+* mismatch (argmax change against the clean prediction, injector.py:318) and
+  detection (any flagged row of the image at the injected layer) are
+  computed on the device and folded into int64 counters per layer, which K5
+  all-reduces across ranks (`distributed.reduce_counters`); nothing but the
+  counters and compact per-trial records leaves the device;
+* sampling follows `sample_injection`'s rules for the output location
+  (injector.py:131-210): per trial an RNG from SeedSequence((seed, layer, k)),
+  per attempt element -> mode -> bit, rejecting no-op flips and corrupted
+  values outside the layer's profiled clean range [lo, hi], at most 64
+  attempts (a trial with none is skipped, as SamplingError skips it in
+  guard.py:705-709).  Attempts are drawn on the host in rounds of four per
+  trial and validated on the device against the clean outputs.  The trial's
+  image is fixed by k (k mod the golden-set size) instead of a drawn sample
+  id, so that a batch holds one trial per image.
+
+Work units are (layer, trial block); `plan_units` balances them over ranks
+by suffix cost (a trial at an early layer recomputes more of the model).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import distributed as Dd
+from . import kernels as K
+from .calib import RunningRange
+
+__all__ = ["ViTCampaign", "CampaignTally", "wilson_interval", "plan_units", "FIELDS", "BF16_FIELDS"]
+
+FIELDS = ("injections", "mismatches", "true_positives", "false_negatives", "benign_detections", "true_negatives",
+          "skipped")
+# (mantissa, exponent) bits per device dtype; bfloat16 is an extension (the reference has no bf16 tag)
+BF16_FIELDS = {torch.bfloat16: (7, 8), torch.float16: (10, 5), torch.float32: (23, 8)}
+MAX_RETRIES = 64  # injector.py:53
+ROUND = 4
+
+
+def wilson_interval(k: int, n: int, z: float = 1.959963984540054) -> tuple[float, float]:
+    """Wilson score interval of a binomial proportion k / n (95% by default)."""
+    if n == 0:
+        return (0.0, 1.0)
+    p = k / n
+    d = 1.0 + z * z / n
+    c = (p + z * z / (2 * n)) / d
+    h = z * math.sqrt(p * (1 - p) / n + z * z / (4 * n * n)) / d
+    return (max(0.0, c - h), min(1.0, c + h))
+
+
+def plan_units(units: list[tuple[int, int]], cost, world_size: int) -> list[list[tuple[int, int]]]:
+    """Greedy longest-first assignment of (layer, block) units to ranks by cost(layer);
+    deterministic (ties by unit order, then rank)."""
+    order = sorted(range(len(units)), key=lambda i: (-cost(units[i][0]), i))
+    load = [0.0] * world_size
+    out: list[list[tuple[int, int]]] = [[] for _ in range(world_size)]
+    for i in order:
+        r = min(range(world_size), key=lambda j: (load[j], j))
+        out[r].append(units[i])
+        load[r] += cost(units[i][0])
+    for o in out:
+        o.sort()
+    return out
+
+
+@dataclass
+class CampaignTally:
+    """Per-layer counters (int64 [n_layers, len(FIELDS)]) plus the clean false-positive audit."""
+
+    counters: np.ndarray
+    clean_checks: int = 0
+    clean_false_positive_checks: int = 0
+    clean_false_positive_inferences: int = 0
+    clean_inferences: int = 0
+    records: dict = field(default_factory=dict)
+
+    def total(self, name: str) -> int:
+        return int(self.counters[:, FIELDS.index(name)].sum())
+
+    @property
+    def coverage(self) -> float:
+        tp, fn = self.total("true_positives"), self.total("false_negatives")
+        return tp / (tp + fn) if tp + fn else 1.0
+
+    def summary(self) -> dict:
+        tp, fn = self.total("true_positives"), self.total("false_negatives")
+        lo, hi = wilson_interval(tp, tp + fn)
+        return {"injections": self.total("injections"), "skipped": self.total("skipped"),
+                "mismatches": self.total("mismatches"), "true_positives": tp, "false_negatives": fn,
+                "benign_detections": self.total("benign_detections"), "true_negatives": self.total("true_negatives"),
+                "coverage_of_mismatches": self.coverage, "coverage_wilson95": [lo, hi],
+                "clean_inferences": self.clean_inferences, "clean_checks": self.clean_checks,
+                "clean_false_positive_checks": self.clean_false_positive_checks,
+                "clean_false_positive_inferences": self.clean_false_positive_inferences,
+                "false_flags_per_image": (self.clean_false_positive_checks / self.clean_inferences
+                                          if self.clean_inferences else 0.0)}
+
+
+def _flip16(bits: torch.Tensor, bit: torch.Tensor) -> torch.Tensor:
+    """XOR one bit of 16-bit encodings (int16 storage), in int32 arithmetic."""
+    v = (bits.to(torch.int32) & 0xFFFF) ^ torch.bitwise_left_shift(torch.ones_like(bit, dtype=torch.int32),
+                                                                      bit.to(torch.int32))
+    return (((v + 32768) & 0xFFFF) - 32768).to(torch.int16)
+
+
+class ViTCampaign:
+    """Output bit-flip campaign over the protected layers of a `ProtectedViT`.
+
+    `images` [G, 3, H, W] on the device is the golden set (one forward batch);
+    the clean pass records predictions, the per-layer clean range of the raw
+    outputs (`gg_minmax`) and the prefix cache; `run` executes trial blocks of
+    G trials per (layer, block)."""
+
+    def __init__(self, model, images: torch.Tensor, *, seed: int = 0,
+                 modes: tuple[str, ...] = ("fp_exponent_bit", "fp_mantissa_bit"), keep_records: bool = False):
+        self.model, self.images, self.seed, self.modes = model, images, seed, modes
+        self.G = images.shape[0]
+        self.dev = images.device
+        self.keep_records = keep_records
+        self.fields = BF16_FIELDS[model.dtype]
+        self.cache: dict = {}
+        with torch.no_grad():
+            logits = model.forward(images, protect=True, cache=self.cache)
+            self.clean_pred = logits.float().argmax(dim=1).clone()
+            self.clean_flags = {i: self._image_flags(i) for i in range(model.cfg.n_layers)}
+            res = model.buffers(self.G).results
+            self._clean_nflag = dict(enumerate(torch.cat([res[i].nflag for i in range(model.cfg.n_layers)])
+                                               .cpu().tolist()))
+            self.ranges = {}
+            self.raw = {}
+            for i in range(model.cfg.n_layers):
+                y = self._raw_output(i)
+                rr = RunningRange(self.dev)
+                rr.update(y)
+                lo, hi, _ = rr.bounds()
+                self.ranges[i] = (lo, hi)
+
+    # ------------------------------------------------------------ helpers
+    def _image_flags(self, i: int) -> torch.Tensor:
+        res = self.model.buffers(self.G).results[i]
+        rows = self.model.rows_per_image(i)
+        return res.flags.view(self.G, rows).any(dim=1)
+
+    def _raw_output(self, i: int) -> torch.Tensor:
+        """Clean raw (pre-activation) output of layer i from its cached input (unprotected launch)."""
+        lin = self.model.layer(i)
+        _, x = self.cache[i]
+        y, _ = K.protected_gemm(x, lin.weight, lin.bias, protect=False, f32_mode=lin.f32_mode, w_split=lin.w_split)
+        return y
+
+    # ------------------------------------------------------------ sampling
+    def _sample(self, layer: int, ks: np.ndarray, y: torch.Tensor):
+        """Element / bit of each trial k (image k % G) by the reference's retry rules; -1 = skipped."""
+        rows = self.model.rows_per_image(layer)
+        N = y.shape[1]
+        n_elem = rows * N
+        mant, exp = self.fields
+        spans = {"fp_mantissa_bit": (0, mant), "fp_exponent_bit": (mant, mant + exp),
+                 "fp_sign_bit": (mant + exp, mant + exp + 1)}
+        rngs = [np.random.default_rng(np.random.SeedSequence((self.seed, layer, int(k)))) for k in ks]
+        n = len(ks)
+        elem = np.full(n, -1, dtype=np.int64)
+        bit = np.zeros(n, dtype=np.int64)
+        mode_ix = np.zeros(n, dtype=np.int64)
+        pending = np.arange(n)
+        lo, hi = self.ranges[layer]
+        img = torch.from_numpy((ks % self.G).astype(np.int64)).to(self.dev)
+        ybits = y.view(torch.int16) if y.element_size() == 2 else y.view(torch.int32)
+        tries = 0
+        while len(pending) and tries < MAX_RETRIES:
+            r = min(ROUND, MAX_RETRIES - tries)
+            ce = np.zeros((len(pending), r), dtype=np.int64)
+            cb = np.zeros((len(pending), r), dtype=np.int64)
+            cm = np.zeros((len(pending), r), dtype=np.int64)
+            for j, t in enumerate(pending):
+                g = rngs[t]
+                for a in range(r):
+                    ce[j, a] = int(g.integers(n_elem))
+                    cm[j, a] = int(g.integers(len(self.modes)))
+                    b0, b1 = spans[self.modes[cm[j, a]]]
+                    cb[j, a] = int(g.integers(b0, b1))
+            pe = torch.from_numpy(ce).to(self.dev)
+            pb = torch.from_numpy(cb).to(self.dev)
+            pimg = img[torch.from_numpy(pending).to(self.dev)].unsqueeze(1)
+            grow = pimg * rows + pe // N
+            gcol = pe % N
+            orig = ybits[grow, gcol]
+            if y.element_size() == 2:
+                flipped = _flip16(orig, pb)
+            else:
+                flipped = orig ^ torch.bitwise_left_shift(torch.ones_like(pb, dtype=torch.int32), pb.to(torch.int32))
+            fv = flipped.view(y.dtype).float()
+            ov = orig.view(y.dtype).float()
+            ok = (fv != ov) & (fv >= lo) & (fv <= hi)  # no-op and range rejection (injector.py:190-196)
+            okh = ok.cpu().numpy()
+            first = np.where(okh.any(axis=1), okh.argmax(axis=1), -1)
+            done = first >= 0
+            sel = pending[done]
+            elem[sel] = ce[done, first[done]]
+            bit[sel] = cb[done, first[done]]
+            mode_ix[sel] = cm[done, first[done]]
+            pending = pending[~done]
+            tries += r
+        return elem, bit, mode_ix
+
+    # ----------------------------------------------------------------- run
+    @torch.no_grad()
+    def run_block(self, layer: int, block: int, counters: torch.Tensor) -> dict | None:
+        """Trials k = block*G .. block*G + G - 1 of `layer`, one per image, folded into counters[layer]."""
+        G = self.G
+        ks = np.arange(block * G, (block + 1) * G, dtype=np.int64)
+        y = self._raw_output(layer)
+        elem, bit, mode_ix = self._sample(layer, ks, y)
+        ok = elem >= 0
+        rows = self.model.rows_per_image(layer)
+        N = y.shape[1]
+        img = ks % G
+        grow = img * rows + np.where(ok, elem // N, 0)
+        gcol = np.where(ok, elem % N, 0)
+        inj = [K.Injection(row=int(r), col=int(c), bit=int(b)) for r, c, b, o in zip(grow, gcol, bit, ok) if o]
+        inj_dev = K.injections_to_device(inj, self.dev)
+        logits = self.model.resume(layer, self.cache, G, protect=True, injections={layer: inj_dev})
+        pred = logits.float().argmax(dim=1)
+        okd = torch.from_numpy(ok).to(self.dev)
+        mism = (pred != self.clean_pred) & okd
+        det = self._image_flags(layer) & okd
+        if not self.model.layer(layer).protected:
+            det = torch.zeros_like(det)
+        row = torch.stack([okd.sum(), mism.sum(), (mism & det).sum(), (mism & ~det).sum(), (~mism & det & okd).sum(),
+                           (~mism & ~det & okd).sum(), (~okd).sum()]).to(torch.int64)
+        counters[layer] += row
+        if not self.keep_records:
+            return None
+        orig_bits = y.view(torch.int16 if y.element_size() == 2 else torch.int32)[
+            torch.from_numpy(grow).to(self.dev), torch.from_numpy(gcol).to(self.dev)]
+        return {"layer": layer, "k": ks, "element": elem, "bit": bit, "mode": mode_ix,
+                "orig_bits": orig_bits.cpu().numpy(), "mismatch": mism.cpu().numpy(), "detected": det.cpu().numpy()}
+
+    def run(self, n_blocks: int, layers=None, *, rank: int = 0, world_size: int = 1) -> CampaignTally:
+        """n_blocks x G trials per layer; units shared over ranks by suffix cost, counters all-reduced (K5)."""
+        nl = self.model.cfg.n_layers
+        layers = list(range(nl)) if layers is None else list(layers)
+        units = [(li, b) for li in layers for b in range(n_blocks)]
+        mine = plan_units(units, lambda li: float(nl - li), world_size)[rank]
+        counters = torch.zeros((nl, len(FIELDS)), dtype=torch.int64, device=self.dev)
+        records = []
+        for li, b in mine:
+            rec = self.run_block(li, b, counters)
+            if rec is not None:
+                records.append(rec)
+        Dd.reduce_counters(counters)
+        audit = self.clean_counts()
+        return CampaignTally(counters=counters.cpu().numpy(), records={"blocks": records}, **audit)
+
+    def clean_counts(self) -> dict:
+        """Clean false-positive audit of the golden batch: rows checked / flagged, images with any flag."""
+        checks = fp_rows = 0
+        any_flag = torch.zeros(self.G, dtype=torch.bool, device=self.dev)
+        for i in range(self.model.cfg.n_layers):
+            if not self.model.layer(i).protected:
+                continue
+            checks += self.G * self.model.rows_per_image(i)
+            fp_rows += int(self._clean_nflag[i])
+            any_flag |= self.clean_flags[i]
+        return {"clean_checks": checks, "clean_false_positive_checks": fp_rows,
+                "clean_false_positive_inferences": int(any_flag.sum().item()), "clean_inferences": self.G}

@@ -356,7 +356,28 @@ __device__ __forceinline__ void stage_row(uint32_t box, int lane, const uint32_t
   }
 }
 
-template <int KIND, int OUT, bool PROTECT, bool CLAIM>
+// Epilogue activations applied to the stored encoding AFTER the observed row sum
+// (the check runs on the raw, rounded GEMM output: guard.py:10-11, model.py:367-368,
+// SURVEY §8(a) a4 (ii)); the activated value is rounded to the output type again.
+enum : int { ACT_NONE = 0, ACT_GELU_TANH = 1 };
+
+// tanh-GELU of an fp32 pair (model._gelu: 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))));
+// tanh on the MUFU pipe (tanh.approx.f32, |rel err| ~2^-11, below bf16 output rounding)
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 gelu_tanh_f32x2(float2 x) {
+  const float2 x2 = mul_f32x2(x, x);
+  const float2 inner = fma_f32x2(mul_f32x2(x2, make_float2(0.044715f, 0.044715f)), x, x);  // x + 0.044715 x^3
+  const float2 u = mul_f32x2(inner, make_float2(0.7978845608028654f, 0.7978845608028654f));
+  const float2 t = make_float2(tanh_approx(u.x), tanh_approx(u.y));
+  const float2 hx = mul_f32x2(x, make_float2(0.5f, 0.5f));
+  return fma_f32x2(hx, t, hx);  // 0.5 x + 0.5 x tanh(u)
+}
+
+template <int KIND, int OUT, bool PROTECT, bool CLAIM, int ACT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gg_protected_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                   const __grid_constant__ CUtensorMap tmC, const Params p) {
@@ -1107,6 +1128,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
         }
         GG_LAP(tr_obs);
+        if constexpr (ACT == ACT_GELU_TANH && OUT16) {  // activation of the checked value, then stored
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 x = (OUT == O_BF16) ? bf16x2_to_f32x2(o[i])
+                                             : __half22float2(*reinterpret_cast<const __half2*>(&o[i]));
+            const float2 g = gelu_tanh_f32x2(x);
+            o[i] = (OUT == O_BF16) ? pack_bf16x2(g.x, g.y) : pack_f16x2(g.x, g.y);
+          }
+        }
         if (c_tma) {
           // coalesced store: this warp's 32 rows x 32 columns through a swizzled smem box + TMA
           uint8_t* boxp = smC + e * CST_BYTES + (OUT16 ? cbuf * 2048 : 0);

@@ -185,13 +185,13 @@ __global__ void replay_prepare_kernel(const uint8_t* rows, int M, int m_tiles, u
 
 // Per device, once per instantiation: the shared-memory opt-in is a per-device
 // function attribute (a process driving several GPUs configures each one).
-template <int KIND, int OUT, bool PROTECT, bool CLAIM>
+template <int KIND, int OUT, bool PROTECT, bool CLAIM, int ACT>
 int configure_instance(int dev) {
   static std::mutex mu;
   static bool done[64] = {false};
   std::lock_guard<std::mutex> lk(mu);
   if (done[dev]) return 0;
-  auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT, CLAIM>;
+  auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT, CLAIM, ACT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES) != cudaSuccess)
     return fail(GG_ECUDA, "cudaFuncSetAttribute(max dynamic smem, pair kernel) failed");
   done[dev] = true;
@@ -214,7 +214,7 @@ int max_coresident_pairs(int dev) {
   static int cache[64] = {0};
   std::lock_guard<std::mutex> lk(mu);
   if (cache[dev]) return cache[dev];
-  auto kern = pair::gg_protected_gemm_pair_kernel<K_BF16, O_BF16, true, false>;
+  auto kern = pair::gg_protected_gemm_pair_kernel<K_BF16, O_BF16, true, false, pair::ACT_NONE>;
   int n = 0;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES) == cudaSuccess) {
     cudaLaunchConfig_t occ{};
@@ -229,14 +229,14 @@ int max_coresident_pairs(int dev) {
   return n;
 }
 
-template <int KIND, int OUT, bool PROTECT, bool CLAIM = false>
+template <int KIND, int OUT, bool PROTECT, bool CLAIM = false, int ACT = pair::ACT_NONE>
 int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p, int grid,
                          cudaStream_t s) {
-  auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT, CLAIM>;
+  auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT, CLAIM, ACT>;
   int dev;
   int rc = current_device(dev);
   if (rc) return rc;
-  rc = configure_instance<KIND, OUT, PROTECT, CLAIM>(dev);
+  rc = configure_instance<KIND, OUT, PROTECT, CLAIM, ACT>(dev);
   if (rc) return rc;
 #ifdef GG_NO_PDL
   kern<<<grid, pair::THREADS, pair::SMEM_BYTES, s>>>(ta, tb, tc, p);
@@ -259,8 +259,14 @@ int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
 }
 
 template <int KIND, int OUT>
-int dispatch_protect(bool protect, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
-                     int grid, cudaStream_t s) {
+int dispatch_protect(bool protect, int act, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                     const Params& p, int grid, cudaStream_t s) {
+  if constexpr ((KIND == K_BF16 && OUT == O_BF16) || (KIND == K_F16 && OUT == O_F16)) {
+    if (act == GG_ACT_GELU_TANH)
+      return protect ? launch_pair_instance<KIND, OUT, true, false, pair::ACT_GELU_TANH>(ta, tb, tc, p, grid, s)
+                     : launch_pair_instance<KIND, OUT, false, false, pair::ACT_GELU_TANH>(ta, tb, tc, p, grid, s);
+  }
+  if (act != GG_ACT_NONE) return fail(GG_EUNSUPPORTED, "protected_gemm: epilogue activation needs bf16 or fp16 outputs");
   if (!protect) return launch_pair_instance<KIND, OUT, false>(ta, tb, tc, p, grid, s);
   if constexpr (KIND == K_TF32) {  // claimed split-band folds (see the kernel)
     if (!p.one_tile && p.n_tiles >= 8) return launch_pair_instance<KIND, OUT, true, true>(ta, tb, tc, p, grid, s);
@@ -430,18 +436,18 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
 
   switch (kind) {
     case K_BF16:
-      rc = out == O_BF16 ? dispatch_protect<K_BF16, O_BF16>(protect, ta, tb, tc, p, grid, s)
-                         : dispatch_protect<K_BF16, O_F32>(protect, ta, tb, tc, p, grid, s);
+      rc = out == O_BF16 ? dispatch_protect<K_BF16, O_BF16>(protect, d->epilogue_act, ta, tb, tc, p, grid, s)
+                         : dispatch_protect<K_BF16, O_F32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
       break;
     case K_F16:
-      rc = out == O_F16 ? dispatch_protect<K_F16, O_F16>(protect, ta, tb, tc, p, grid, s)
-                        : dispatch_protect<K_F16, O_F32>(protect, ta, tb, tc, p, grid, s);
+      rc = out == O_F16 ? dispatch_protect<K_F16, O_F16>(protect, d->epilogue_act, ta, tb, tc, p, grid, s)
+                        : dispatch_protect<K_F16, O_F32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
       break;
     case K_TF32:
-      rc = dispatch_protect<K_TF32, O_F32>(protect, ta, tb, tc, p, grid, s);
+      rc = dispatch_protect<K_TF32, O_F32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
       break;
     default:
-      rc = dispatch_protect<K_I8, O_I32>(protect, ta, tb, tc, p, grid, s);
+      rc = dispatch_protect<K_I8, O_I32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
   }
   if (rc == 0 && batch_mean)
     rc = launch_batch_mean_finish(d->M, d->mu, d->lo, d->hi, static_cast<const double*>(d->d), d->flags, d->max_disc,

@@ -286,6 +286,14 @@ __device__ __forceinline__ float2 fma_f32x2(float2 a, float2 b, float2 c) {
         "l"(*reinterpret_cast<unsigned long long*>(&c)));
   return *reinterpret_cast<float2*>(&r);
 }
+// packed fp32 pair multiply (sm_100: FMUL2)
+__device__ __forceinline__ float2 mul_f32x2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
 // packed bf16 pair -> two fp32 (lo from bits 0-15) on the ALU pipe (PRMT + LOP3, no IMAD)
 __device__ __forceinline__ float2 bf16x2_to_f32x2(uint32_t w) {
   return make_float2(__uint_as_float(__byte_perm(w, 0u, 0x1054u)), __uint_as_float(w & 0xFFFF0000u));

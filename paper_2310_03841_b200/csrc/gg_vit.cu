@@ -1,0 +1,177 @@
+// gg_vit.cu — the transformer glue between the protected GEMMs of the ViT /
+// Swin forward (unprotected: only the Linear layers carry
+// checksums).  HBM-bound elementwise / row work, one pass each:
+//
+//   gg_add_layernorm   h <- h + y (residual update, optional) and a = LN(h) * gamma + beta
+//                      in one read of h, y and one write of h, a (fp32 statistics)
+//
+// One warp per row, 16-byte vector accesses, the row held in registers
+// between the statistics and the normalisation (two-pass mean / variance).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gg_internal.h"
+
+namespace gg {
+namespace {
+
+template <typename T>
+struct Vec;  // 16 bytes of T
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ static void load(const void* p, float (&v)[8]) {
+    const uint4 u = *static_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+  __device__ static void store(void* p, const float (&v)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+    *static_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <>
+struct Vec<__half> {
+  static constexpr int N = 8;
+  __device__ static void load(const void* p, float (&v)[8]) {
+    const uint4 u = *static_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      v[2 * i] = f.x;
+      v[2 * i + 1] = f.y;
+    }
+  }
+  __device__ static void store(void* p, const float (&v)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    *static_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ static void load(const void* p, float (&v)[4]) {
+    const float4 u = *static_cast<const float4*>(p);
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+  }
+  __device__ static void store(void* p, const float (&v)[4]) {
+    *static_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+
+// CH = 16-byte chunks per lane (D = 32 * CH * Vec::N)
+template <typename T, int CH>
+// h_out may alias h (in-place residual update): neither is __restrict__.
+__global__ void __launch_bounds__(256) add_layernorm_kernel(const T* h, const T* __restrict__ y, int64_t rows, int D,
+                                                            const float* __restrict__ gamma,
+                                                            const float* __restrict__ beta, float eps, T* h_out,
+                                                            T* __restrict__ ln_out) {
+  constexpr int V = Vec<T>::N;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const T* hr = h + row * D;
+  float v[CH][V];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int col = (c * 32 + lane) * V;
+    Vec<T>::load(hr + col, v[c]);
+    if (y != nullptr) {
+      float t[V];
+      Vec<T>::load(y + row * D + col, t);
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[c][i] += t[i];
+      uint4 packed;  // the stored (rounded) residual is what LN sees
+      Vec<T>::store(&packed, v[c]);
+      Vec<T>::load(&packed, v[c]);
+      *reinterpret_cast<uint4*>(h_out + row * D + col) = packed;
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+#pragma unroll
+    for (int i = 0; i < V; ++i) s += v[c][i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / static_cast<float>(D);
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float dv = v[c][i] - mean;
+      q += dv * dv;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / static_cast<float>(D) + eps);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int col = (c * 32 + lane) * V;
+    float o[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) o[i] = (v[c][i] - mean) * rstd * gamma[col + i] + beta[col + i];
+    Vec<T>::store(ln_out + row * D + col, o);
+  }
+}
+
+template <typename T>
+int launch_add_ln_t(const void* h, const void* y, int64_t rows, int D, const float* gamma, const float* beta,
+                    float eps, void* h_out, void* ln_out, cudaStream_t s) {
+  constexpr int V = Vec<T>::N;
+  if (D % (32 * V) != 0) return fail(GG_EUNSUPPORTED, "add_layernorm: D must be a multiple of 32 x 16 bytes");
+  const int ch = D / (32 * V);
+  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+  const T* hp = static_cast<const T*>(h);
+  const T* yp = static_cast<const T*>(y);
+  T* ho = static_cast<T*>(h_out);
+  T* lo = static_cast<T*>(ln_out);
+  switch (ch) {
+#define GG_LN_CASE(n) \
+  case n: add_layernorm_kernel<T, n><<<grid, 256, 0, s>>>(hp, yp, rows, D, gamma, beta, eps, ho, lo); break;
+    GG_LN_CASE(1) GG_LN_CASE(2) GG_LN_CASE(3) GG_LN_CASE(4) GG_LN_CASE(5) GG_LN_CASE(6) GG_LN_CASE(8)
+#undef GG_LN_CASE
+    default:
+      return fail(GG_EUNSUPPORTED, "add_layernorm: row width not built (32 x 16-byte chunks x {1..6, 8})");
+  }
+  return check_launch("add_layernorm");
+}
+
+}  // namespace
+
+int launch_add_layernorm(int dtype, const void* h, const void* y, int64_t rows, int64_t D, const float* gamma,
+                         const float* beta, float eps, void* h_out, void* ln_out, cudaStream_t s) {
+  if (rows < 1 || D < 1) return fail(GG_EINVAL, "add_layernorm: empty input");
+  if (gamma == nullptr || beta == nullptr || ln_out == nullptr) return fail(GG_EINVAL, "add_layernorm: null argument");
+  if (y != nullptr && h_out == nullptr) return fail(GG_EINVAL, "add_layernorm: residual update needs h_out");
+  if ((reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(h_out) |
+       reinterpret_cast<uintptr_t>(ln_out)) & 15)
+    return fail(GG_EINVAL, "add_layernorm: tensors must be 16-byte aligned");
+  switch (dtype) {
+    case GG_BF16: return launch_add_ln_t<__nv_bfloat16>(h, y, rows, static_cast<int>(D), gamma, beta, eps, h_out, ln_out, s);
+    case GG_F16: return launch_add_ln_t<__half>(h, y, rows, static_cast<int>(D), gamma, beta, eps, h_out, ln_out, s);
+    case GG_F32: return launch_add_ln_t<float>(h, y, rows, static_cast<int>(D), gamma, beta, eps, h_out, ln_out, s);
+    default: return fail(GG_EUNSUPPORTED, "add_layernorm: dtype must be GG_BF16, GG_F16 or GG_F32");
+  }
+}
+
+}  // namespace gg

@@ -153,6 +153,7 @@ def build_desc(
     ws: torch.Tensor | None = None,
     replay_rows: torch.Tensor | None = None,
     changed: torch.Tensor | None = None,
+    act: int = L.GG_ACT_NONE,
 ) -> L.GGGemmDesc:
     M, K = x.shape
     N = w.shape[0]
@@ -186,6 +187,7 @@ def build_desc(
     d.n_inj = int(n_inj)
     d.replay_rows = _ptr(replay_rows)
     d.changed = _ptr(changed)
+    d.epilogue_act = int(act)
     return d
 
 
@@ -301,12 +303,14 @@ def protected_gemm(
     ws_key=None,
     f32_mode: str = "3xtf32",
     w_split: torch.Tensor | None = None,
+    act: int = L.GG_ACT_NONE,
 ) -> tuple[torch.Tensor, CheckResult | None]:
     """K1: y = x @ w.T + bias with the fused checksum check (one launch).
 
     x [M, K], w [N, K] (torch Linear layout), bias [N] (f32, or i32 for int8).
     fp32 operands run as 3xTF32 (binary32 accuracy; `w_split` may hold the
     weight's cached `split_tf32x3(w, 1)`) unless f32_mode="tf32" (one tf32 pass).
+    act=GG_ACT_GELU_TANH stores GELU(y) (16-bit outputs) after the check of y.
     Returns (y, CheckResult or None when protect=False).
     """
     dev = _require_cuda(x, w, bias)
@@ -329,7 +333,7 @@ def protected_gemm(
     else:
         inj_dev, n_inj = None, 0
     desc = build_desc(x, w, y, bias, protect=protect, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo,
-                      hi=hi, statistic=statistic, result=result, inj_dev=inj_dev, n_inj=n_inj, ws=ws)
+                      hi=hi, statistic=statistic, result=result, inj_dev=inj_dev, n_inj=n_inj, ws=ws, act=act)
     L.check(L.load().gg_protected_gemm(ctypes.byref(desc), _stream(dev)), "gg_protected_gemm")
     return y, (result if protect else None)
 
@@ -400,6 +404,7 @@ def replay_tiles(
     ws_key=None,
     f32_mode: str = "3xtf32",
     w_split: torch.Tensor | None = None,
+    act: int = L.GG_ACT_NONE,
 ) -> torch.Tensor:
     """K4: recompute only the M-bands holding a flagged row, in place in y.
 
@@ -414,7 +419,7 @@ def replay_tiles(
     changed = changed if changed is not None else torch.zeros(1, dtype=torch.int32, device=dev)
     ws = workspace(M, N, dev, ws_key)
     desc = build_desc(x, w, y, bias, protect=True, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
-                      statistic=statistic, result=result, ws=ws, replay_rows=replay_rows, changed=changed)
+                      statistic=statistic, result=result, ws=ws, replay_rows=replay_rows, changed=changed, act=act)
     L.check(L.load().gg_replay_tiles(ctypes.byref(desc), _stream(dev)), "gg_replay_tiles")
     return changed
 
@@ -517,3 +522,16 @@ def reduce(a: torch.Tensor, axis: int) -> torch.Tensor:
     L.check(L.load().gg_reduce(TORCH_TO_GG[a.dtype], a.data_ptr(), rows, cols, axis, out.data_ptr(), _stream(dev)),
             "gg_reduce")
     return out
+
+
+def add_layernorm(h: torch.Tensor, y: torch.Tensor | None, gamma: torch.Tensor, beta: torch.Tensor, eps: float,
+                  ln_out: torch.Tensor, h_out: torch.Tensor | None = None) -> None:
+    """gg_add_layernorm: h_out = h + y (if y is given; h_out may be h), ln_out = LN(.) * gamma + beta."""
+    dev = _require_cuda(h, y, gamma, beta, ln_out, h_out)
+    rows, D = h.shape
+    for t in (h, y, ln_out, h_out):
+        if t is not None and (not t.is_contiguous() or t.shape != (rows, D) or t.dtype != h.dtype):
+            raise ValueError("add_layernorm takes contiguous [rows, D] tensors of one dtype")
+    L.check(L.load().gg_add_layernorm(TORCH_TO_GG[h.dtype], h.data_ptr(), _ptr(y), rows, D, gamma.data_ptr(),
+                                      beta.data_ptr(), float(eps), _ptr(h_out), ln_out.data_ptr(), _stream(dev)),
+            "gg_add_layernorm")
