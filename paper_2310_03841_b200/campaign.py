@@ -103,6 +103,18 @@ class CampaignTally:
         tp, fn = self.total("true_positives"), self.total("false_negatives")
         return tp / (tp + fn) if tp + fn else 1.0
 
+    def by_group(self, groups: dict[str, list[int]]) -> dict:
+        """Coverage per group of layers (e.g. the ViT roles): {name: [mismatches, TP, FN, coverage]}."""
+        out = {}
+        c = self.counters
+        for name, idx in groups.items():
+            mm = int(c[idx, FIELDS.index("mismatches")].sum())
+            tp = int(c[idx, FIELDS.index("true_positives")].sum())
+            fn = int(c[idx, FIELDS.index("false_negatives")].sum())
+            out[name] = {"mismatches": mm, "true_positives": tp, "false_negatives": fn,
+                         "coverage": tp / (tp + fn) if tp + fn else 1.0}
+        return out
+
     def summary(self) -> dict:
         tp, fn = self.total("true_positives"), self.total("false_negatives")
         lo, hi = wilson_interval(tp, tp + fn)
@@ -160,7 +172,7 @@ class ViTCampaign:
     def _image_flags(self, i: int) -> torch.Tensor:
         res = self.model.buffers(self.G).results[i]
         rows = self.model.rows_per_image(i)
-        return res.flags.view(self.G, rows).any(dim=1)
+        return res.flags.view(self.G, rows).bool().any(dim=1)
 
     def _raw_output(self, i: int) -> torch.Tensor:
         """Clean raw (pre-activation) output of layer i from its cached input (unprotected launch)."""

@@ -414,6 +414,15 @@ class ProtectedViT(torch.nn.Module):
                 lin.set_epsilon(0.0, 0.0, 0.0)
         return out
 
+    def role_groups(self) -> dict[str, list[int]]:
+        """Layer indices by role: patch_embed, qkv, proj, fc1, fc2, head."""
+        d = self.cfg.depth
+        groups = {"patch_embed": [0]}
+        for j, role in enumerate(LAYER_ROLES):
+            groups[role] = [1 + 4 * b + j for b in range(d)]
+        groups["head"] = [self.cfg.n_layers - 1]
+        return groups
+
     def flagged_rows(self, B: int) -> torch.Tensor:
         """Device int64 [n_layers]: flagged rows of the last forward's checks per layer."""
         bf = self.buffers(B)
