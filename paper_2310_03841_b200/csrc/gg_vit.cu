@@ -127,9 +127,16 @@ __global__ void __launch_bounds__(256) add_layernorm_kernel(const T* h, const T*
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     const int col = (c * 32 + lane) * V;
-    float o[V];
+    float gm[V], bt[V], o[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) o[i] = (v[c][i] - mean) * rstd * gamma[col + i] + beta[col + i];
+    for (int i = 0; i < V; i += 4) {  // 16-byte loads of the (L1-resident) affine parameters
+      const float4 g4 = __ldg(reinterpret_cast<const float4*>(gamma + col + i));
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(beta + col + i));
+      gm[i] = g4.x; gm[i + 1] = g4.y; gm[i + 2] = g4.z; gm[i + 3] = g4.w;
+      bt[i] = b4.x; bt[i + 1] = b4.y; bt[i + 2] = b4.z; bt[i + 3] = b4.w;
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) o[i] = fmaf((v[c][i] - mean) * rstd, gm[i], bt[i]);
     Vec<T>::store(ln_out + row * D + col, o);
   }
 }
@@ -164,7 +171,8 @@ int launch_add_layernorm(int dtype, const void* h, const void* y, int64_t rows, 
   if (gamma == nullptr || beta == nullptr || ln_out == nullptr) return fail(GG_EINVAL, "add_layernorm: null argument");
   if (y != nullptr && h_out == nullptr) return fail(GG_EINVAL, "add_layernorm: residual update needs h_out");
   if ((reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(h_out) |
-       reinterpret_cast<uintptr_t>(ln_out)) & 15)
+       reinterpret_cast<uintptr_t>(ln_out) | reinterpret_cast<uintptr_t>(gamma) | reinterpret_cast<uintptr_t>(beta)) &
+      15)
     return fail(GG_EINVAL, "add_layernorm: tensors must be 16-byte aligned");
   switch (dtype) {
     case GG_BF16: return launch_add_ln_t<__nv_bfloat16>(h, y, rows, static_cast<int>(D), gamma, beta, eps, h_out, ln_out, s);

@@ -183,6 +183,7 @@ class _Buffers:
     cls_in: torch.Tensor
     logits: torch.Tensor
     results: dict = field(default_factory=dict)
+    o_view: torch.Tensor | None = None  # the proj input: the attention output itself when contiguous, else o
 
 
 class ProtectedViT(torch.nn.Module):
@@ -269,8 +270,12 @@ class ProtectedViT(torch.nn.Module):
         hd = c.dim // H
         qkv = bf.qkv.view(B, T, 3, H, hd)
         q, k, v = (qkv[:, :, j].transpose(1, 2) for j in range(3))
-        o = F.scaled_dot_product_attention(q, k, v)
-        bf.o.view(B, T, H, hd).copy_(o.transpose(1, 2))
+        o = F.scaled_dot_product_attention(q, k, v).transpose(1, 2)
+        if o.is_contiguous():  # the attention kernel wrote [B, T, H, hd]: the proj input is a view
+            bf.o_view = o.view(B * T, c.dim)
+        else:
+            bf.o.view(B, T, H, hd).copy_(o)
+            bf.o_view = bf.o
 
     def _ln(self, j: int):
         return self.ln_g[j], self.ln_b[j]
@@ -327,8 +332,9 @@ class ProtectedViT(torch.nn.Module):
             if start <= base + 1:
                 if start == base + 1:
                     load(base + 1, h, bf.o)
-                save(base + 1, h, bf.o)
-                self._lin(base + 1, bf.o, bf.y, bf, protect, inj)
+                    bf.o_view = bf.o
+                save(base + 1, h, bf.o_view)
+                self._lin(base + 1, bf.o_view, bf.y, bf, protect, inj)
                 K.add_layernorm(h, bf.y, *self._ln(2 * b + 1), eps, ln_out=a, h_out=h)
             if start <= base + 2:
                 if start == base + 2:
