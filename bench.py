@@ -228,6 +228,18 @@ def _timed(fn, steps, warmup, world, dev, stream):
 _CAPTURE_STREAM = None
 
 
+def _interleaved(fa, fb, rounds, steps, warmup, world, dev, stream):
+    """Median per-step times of two step functions timed in alternating rounds (A B, B A, ...)
+    so that clock / power drift under the power cap hits both equally."""
+    ta, tb = [], []
+    for r in range(rounds):
+        order = (fa, fb) if r % 2 == 0 else (fb, fa)
+        for f in order:
+            ms = _timed(f, steps, warmup if r == 0 else 1, world, dev, stream)
+            (ta if f is fa else tb).append(ms)
+    return statistics.median(ta), statistics.median(tb)
+
+
 def _capture(fn):
     """CUDA graph of fn, warmed on the capture stream itself so that per-stream
     workspaces (kernels.workspace) are allocated and zeroed outside the graph."""
@@ -285,8 +297,7 @@ def gemm_only(args, dev, world, stream):
         ly["mu"], ly["lo"], ly["hi"] = stats[ly["name"]].epsilon(CONFIDENCE)
     gp = _capture(lambda: [launch(ly, True) for ly in layers])
     gu = _capture(lambda: [launch(ly, False) for ly in layers])
-    ms_p = _timed(gp.replay, args.steps, args.warmup, world, dev, stream)
-    ms_u = _timed(gu.replay, args.steps, args.warmup, world, dev, stream)
+    ms_p, ms_u = _interleaved(gp.replay, gu.replay, 6, max(3, args.steps // 2), args.warmup, world, dev, stream)
     flops = gemm_flops(gemms)
     out = {"protected_gemm_tflops": flops / (ms_p * 1e-3) / 1e12, "unprotected_gemm_tflops": flops / (ms_u * 1e-3) / 1e12,
            "gemm_overhead_pct": 100.0 * (ms_p / ms_u - 1.0), "gemm_ms_per_step": ms_p,
@@ -322,7 +333,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict:
         g_u = _capture(fwd_u)
         with ClockSampler(local_rank) as clk:
             ms_p = _timed(g_p.replay, args.steps, args.warmup, world, dev, stream)
-        ms_u = _timed(g_u.replay, args.steps, args.warmup, world, dev, stream)
+        # overhead: protected vs unprotected forward in alternating rounds (median per step)
+        ab_p, ab_u = _interleaved(g_p.replay, g_u.replay, 6, max(3, args.steps // 2), args.warmup, world, dev, stream)
         g_p.replay()
         flagged = model.flagged_rows(BATCH)  # held-out false flags of the timed batch (K5 over NCCL)
         if world > 1:
@@ -338,7 +350,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict:
 
     gemm_f, attn_f = cfg.flops_per_image()
     img_s = BATCH * world / (ms_p * 1e-3)
-    img_s_u = BATCH * world / (ms_u * 1e-3)
+    img_s_u = BATCH * world / (ab_u * 1e-3)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("bf16_tflops_sustained") or 1400.0
     k1 = gem["protected_gemm_tflops"] / world
@@ -353,7 +365,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict:
                    "seq_len": TOKENS, "protected_gemms": layer_launches, "parallelism": f"replicas{world}",
                    "epsilon": f"per-layer mu +/- z*sigma, c={CONFIDENCE}",
                    "l2": "one step moves ~15 GB of activations (>> 126 MB L2)"},
-        "overhead_pct": 100.0 * (ms_p / ms_u - 1.0), "unprotected_img_per_s": img_s_u,
+        "overhead_pct": 100.0 * (ab_p / ab_u - 1.0), "unprotected_img_per_s": img_s_u,
+        "overhead_method": "protected vs unprotected forward graphs, 6 alternating rounds, median ms per step",
         "protected_gemm_tflops": gem["protected_gemm_tflops"], "gemm_overhead_pct": gem["gemm_overhead_pct"],
         "gemm_only": gem,
         "held_out_false_flags": false_flags,
@@ -383,28 +396,40 @@ def coverage_study(model, held, images, args, rank, world, dev) -> dict:
     from paper_2310_03841_b200.campaign import ViTCampaign
     from paper_2310_03841_b200.vit import VIT_B16, ProtectedViT
 
-    out = {}
+    from paper_2310_03841_b200.campaign import select_golden_images
 
-    def one(m, imgs, c, cal, tag):
+    out = {}
+    # golden set: images the bf16 model classifies like its fp32 teacher (profiler.select_golden's rule)
+    teacher = ProtectedViT(VIT_B16, dtype=torch.float32, device=dev, seed=1234, f32_mode="3xtf32")
+    golden, gstats = select_golden_images(model, teacher, images, BATCH)
+    out["golden"] = gstats
+    del teacher
+    torch.cuda.empty_cache()
+
+    def one(m, imgs, c, cal, tag, modes=("fp_exponent_bit", "fp_mantissa_bit")):
         m.calibrate(cal, c)
         t0 = time.perf_counter()
-        camp = ViTCampaign(m, imgs, seed=2310)
+        camp = ViTCampaign(m, imgs, seed=2310, modes=modes)
         tally = camp.run(args.campaign_blocks, rank=rank, world_size=world)
         torch.cuda.synchronize()
         s = tally.summary()
         s["trials_per_s"] = s["injections"] / (time.perf_counter() - t0)
         s["confidence"] = c
+        s["modes"] = list(modes)
         s["by_role"] = tally.by_group(m.role_groups())
         out[tag] = s
         del camp
 
     cal = [images(), images()]
-    one(model, held, CONFIDENCE, cal, f"bf16 c={CONFIDENCE}")
-    one(model, held, 0.9999, cal, "bf16 c=0.9999")
+    one(model, golden, CONFIDENCE, cal, f"bf16 c={CONFIDENCE} bit flips")
+    one(model, golden, CONFIDENCE, cal, f"bf16 c={CONFIDENCE} random values", ("random_value",))
+    one(model, golden, 0.9999, cal, "bf16 c=0.9999 random values", ("random_value",))
+    one(model, held, CONFIDENCE, cal, f"bf16 c={CONFIDENCE} bit flips, unfiltered images (near-ties kept)")
     model.calibrate(cal, CONFIDENCE)
     torch.cuda.empty_cache()
     m16 = ProtectedViT(VIT_B16, dtype=torch.float16, device=dev, seed=1234)
-    one(m16, held.to(torch.float16), CONFIDENCE, [c.to(torch.float16) for c in cal], f"fp16 c={CONFIDENCE}")
+    one(m16, golden.to(torch.float16), CONFIDENCE, [c.to(torch.float16) for c in cal],
+        f"fp16 c={CONFIDENCE} random values", ("random_value",))
     del m16
     torch.cuda.empty_cache()
     return out

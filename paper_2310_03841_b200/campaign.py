@@ -48,7 +48,8 @@ from . import distributed as Dd
 from . import kernels as K
 from .calib import RunningRange
 
-__all__ = ["ViTCampaign", "CampaignTally", "wilson_interval", "plan_units", "FIELDS", "BF16_FIELDS"]
+__all__ = ["ViTCampaign", "CampaignTally", "wilson_interval", "plan_units", "select_golden_images", "FIELDS",
+           "BF16_FIELDS"]
 
 FIELDS = ("injections", "mismatches", "true_positives", "false_negatives", "benign_detections", "true_negatives",
           "skipped")
@@ -129,6 +130,39 @@ class CampaignTally:
                                           if self.clean_inferences else 0.0)}
 
 
+@torch.no_grad()
+def select_golden_images(model, teacher, make_batch, B: int, max_batches: int = 8) -> tuple[torch.Tensor, dict]:
+    """Golden set of B images (profiler.select_golden, profiler.py:83-96): synthetic
+    images labelled by a teacher (make_synthetic_dataset's teacher labelling,
+    model.py:238-254) — here the same network at full precision (fp32 weights,
+    binary32 GEMMs) — of which the deployed low-precision model keeps the ones it
+    classifies correctly AND unambiguously: its top-2 logits more than two output
+    ulps apart (a bf16 tie broken by argmax's index order is not a
+    classification, and any perturbation would "mismatch" it).
+    Returns (images [B, ...] on the device, stats)."""
+    kept, seen, ties = [], 0, 0
+    for _ in range(max_batches):
+        imgs = make_batch()
+        lab = teacher(imgs.to(teacher.dtype)).float().argmax(dim=1)
+        lg = model(imgs)
+        top2 = lg.float().topk(2, dim=1).values
+        ulp = (top2[:, 0].abs() * 2.0 ** -(BF16_FIELDS[lg.dtype][0])).clamp_min(2.0 ** -24)
+        clear = (top2[:, 0] - top2[:, 1]) > 2 * ulp
+        ties += int((~clear).sum().item())
+        ok = ((lab == lg.float().argmax(dim=1)) & clear).nonzero().flatten()
+        kept.append(imgs[ok].clone())
+        seen += imgs.shape[0]
+        if sum(k.shape[0] for k in kept) >= B:
+            break
+    pool = torch.cat(kept)
+    if pool.shape[0] < B:
+        raise ValueError(f"only {pool.shape[0]} of {seen} images are classified like the teacher")
+    return pool[:B].contiguous(), {"candidates": seen, "golden": int(pool.shape[0]),
+                                   "golden_fraction": pool.shape[0] / seen, "near_ties_excluded": ties,
+                                   "teacher": "same weights in fp32 (binary32 GEMMs)",
+                                   "rule": "teacher label == model argmax and top-2 gap > 2 output ulps"}
+
+
 def _flip16(bits: torch.Tensor, bit: torch.Tensor) -> torch.Tensor:
     """XOR one bit of 16-bit encodings (int16 storage), in int32 arithmetic."""
     v = (bits.to(torch.int32) & 0xFFFF) ^ torch.bitwise_left_shift(torch.ones_like(bit, dtype=torch.int32),
@@ -183,46 +217,59 @@ class ViTCampaign:
 
     # ------------------------------------------------------------ sampling
     def _sample(self, layer: int, ks: np.ndarray, y: torch.Tensor):
-        """Element / bit of each trial k (image k % G) by the reference's retry rules; -1 = skipped."""
+        """Element / bit (or value) of each trial k (image k % G) by the reference's retry
+        rules (injector.py:131-210); elem -1 = skipped.  Bit modes flip a bit of the
+        stored encoding; "random_value" draws uniform(lo, hi) and stores it rounded
+        to the output type.  Returns (elem, bit (-1 for value modes), mode index, value)."""
         rows = self.model.rows_per_image(layer)
         N = y.shape[1]
         n_elem = rows * N
         mant, exp = self.fields
         spans = {"fp_mantissa_bit": (0, mant), "fp_exponent_bit": (mant, mant + exp),
                  "fp_sign_bit": (mant + exp, mant + exp + 1)}
+        for m in self.modes:
+            if m not in spans and m != "random_value":
+                raise ValueError(f"campaign mode {m!r} is not supported on the device engine")
         rngs = [np.random.default_rng(np.random.SeedSequence((self.seed, layer, int(k)))) for k in ks]
         n = len(ks)
         elem = np.full(n, -1, dtype=np.int64)
-        bit = np.zeros(n, dtype=np.int64)
+        bit = np.full(n, -1, dtype=np.int64)
         mode_ix = np.zeros(n, dtype=np.int64)
+        value = np.zeros(n, dtype=np.float64)
         pending = np.arange(n)
         lo, hi = self.ranges[layer]
         img = torch.from_numpy((ks % self.G).astype(np.int64)).to(self.dev)
-        ybits = y.view(torch.int16) if y.element_size() == 2 else y.view(torch.int32)
+        wide = y.element_size() == 2
+        ybits = y.view(torch.int16) if wide else y.view(torch.int32)
         tries = 0
         while len(pending) and tries < MAX_RETRIES:
             r = min(ROUND, MAX_RETRIES - tries)
             ce = np.zeros((len(pending), r), dtype=np.int64)
-            cb = np.zeros((len(pending), r), dtype=np.int64)
+            cb = np.full((len(pending), r), -1, dtype=np.int64)
             cm = np.zeros((len(pending), r), dtype=np.int64)
+            cv = np.zeros((len(pending), r), dtype=np.float64)
             for j, t in enumerate(pending):
                 g = rngs[t]
-                for a in range(r):
+                for a in range(r):  # draw order of injector.py:169-186: element, mode, bit | value
                     ce[j, a] = int(g.integers(n_elem))
                     cm[j, a] = int(g.integers(len(self.modes)))
-                    b0, b1 = spans[self.modes[cm[j, a]]]
-                    cb[j, a] = int(g.integers(b0, b1))
+                    mode = self.modes[cm[j, a]]
+                    if mode == "random_value":
+                        cv[j, a] = float(g.uniform(lo, hi))
+                    else:
+                        b0, b1 = spans[mode]
+                        cb[j, a] = int(g.integers(b0, b1))
             pe = torch.from_numpy(ce).to(self.dev)
             pb = torch.from_numpy(cb).to(self.dev)
             pimg = img[torch.from_numpy(pending).to(self.dev)].unsqueeze(1)
             grow = pimg * rows + pe // N
             gcol = pe % N
             orig = ybits[grow, gcol]
-            if y.element_size() == 2:
-                flipped = _flip16(orig, pb)
-            else:
-                flipped = orig ^ torch.bitwise_left_shift(torch.ones_like(pb, dtype=torch.int32), pb.to(torch.int32))
-            fv = flipped.view(y.dtype).float()
+            isbit = pb >= 0
+            sh = torch.bitwise_left_shift(torch.ones_like(pb, dtype=torch.int32), pb.clamp_min(0).to(torch.int32))
+            flipped = _flip16(orig, pb.clamp_min(0)) if wide else orig ^ sh
+            fv = torch.where(isbit, flipped.view(y.dtype).float(),
+                             torch.from_numpy(cv).to(self.dev).to(y.dtype).float())  # value rounded like the store
             ov = orig.view(y.dtype).float()
             ok = (fv != ov) & (fv >= lo) & (fv <= hi)  # no-op and range rejection (injector.py:190-196)
             okh = ok.cpu().numpy()
@@ -232,9 +279,10 @@ class ViTCampaign:
             elem[sel] = ce[done, first[done]]
             bit[sel] = cb[done, first[done]]
             mode_ix[sel] = cm[done, first[done]]
+            value[sel] = cv[done, first[done]]
             pending = pending[~done]
             tries += r
-        return elem, bit, mode_ix
+        return elem, bit, mode_ix, value
 
     # ----------------------------------------------------------------- run
     @torch.no_grad()
@@ -243,14 +291,16 @@ class ViTCampaign:
         G = self.G
         ks = np.arange(block * G, (block + 1) * G, dtype=np.int64)
         y = self._raw_output(layer)
-        elem, bit, mode_ix = self._sample(layer, ks, y)
+        elem, bit, mode_ix, value = self._sample(layer, ks, y)
         ok = elem >= 0
         rows = self.model.rows_per_image(layer)
         N = y.shape[1]
         img = ks % G
         grow = img * rows + np.where(ok, elem // N, 0)
         gcol = np.where(ok, elem % N, 0)
-        inj = [K.Injection(row=int(r), col=int(c), bit=int(b)) for r, c, b, o in zip(grow, gcol, bit, ok) if o]
+        inj = [K.Injection(row=int(r), col=int(c), bit=int(b)) if b >= 0 else
+               K.Injection(row=int(r), col=int(c), mode=L.GG_INJ_SET_VALUE, value=float(v))
+               for r, c, b, v, o in zip(grow, gcol, bit, value, ok) if o]
         inj_dev = K.injections_to_device(inj, self.dev)
         logits = self.model.resume(layer, self.cache, G, protect=True, injections={layer: inj_dev})
         pred = logits.float().argmax(dim=1)
@@ -266,7 +316,7 @@ class ViTCampaign:
             return None
         orig_bits = y.view(torch.int16 if y.element_size() == 2 else torch.int32)[
             torch.from_numpy(grow).to(self.dev), torch.from_numpy(gcol).to(self.dev)]
-        return {"layer": layer, "k": ks, "element": elem, "bit": bit, "mode": mode_ix,
+        return {"layer": layer, "k": ks, "element": elem, "bit": bit, "mode": mode_ix, "value": value,
                 "orig_bits": orig_bits.cpu().numpy(), "mismatch": mism.cpu().numpy(), "detected": det.cpu().numpy()}
 
     def run(self, n_blocks: int, layers=None, *, rank: int = 0, world_size: int = 1) -> CampaignTally:

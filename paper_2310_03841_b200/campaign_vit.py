@@ -29,7 +29,7 @@ import torch
 import torch.distributed as dist
 
 from . import calib
-from .campaign import FIELDS, ViTCampaign, wilson_interval
+from .campaign import FIELDS, ViTCampaign, select_golden_images, wilson_interval
 from .vit import VIT_B16, VIT_L16, ProtectedViT, ViTConfig
 
 MODELS = {"vit_b16": VIT_B16, "vit_l16": VIT_L16}
@@ -77,7 +77,14 @@ def run(args) -> dict | None:
     gold_g = torch.Generator(device=dev).manual_seed(7)  # the same golden batch on every rank
     mk = lambda gen: torch.randn(args.batch, 3, cfg.image, cfg.image, device=dev, generator=gen).to(dtype)  # noqa: E731
     calibrate_distributed(model, [mk(g) for _ in range(args.cal_batches)], args.confidence)
-    golden = mk(gold_g)
+    gstats = {"selection": "random synthetic images (no teacher filter)"}
+    if args.teacher:
+        teacher = ProtectedViT(cfg, dtype=torch.float32, device=dev, seed=args.seed, f32_mode="3xtf32")
+        golden, gstats = select_golden_images(model, teacher, lambda: mk(gold_g), args.batch)
+        del teacher
+        torch.cuda.empty_cache()
+    else:
+        golden = mk(gold_g)
     camp = ViTCampaign(model, golden, seed=args.seed)
     n_layers = cfg.n_layers
     per_layer = math.ceil(args.trials / n_layers)
@@ -114,7 +121,7 @@ def run(args) -> dict | None:
             "skipped": summ["skipped"], "blocks_per_layer": n_blocks, "images_per_block": args.batch,
             "device_s": s, "wall_s": wall, "trials_per_s": summ["injections"] / s,
             "full_forward_flop_per_trial": gemm_f + attn_f, "confidence": args.confidence,
-            "summary": summ, "by_role": roles,
+            "summary": summ, "by_role": roles, "golden": gstats,
             "scope": "one output bit flip per image of a 256-image batch at one protected layer, prefix reuse "
                      "(forward resumed at the layer), range-constrained exponent/mantissa flips, mismatch = "
                      "argmax change vs the clean prediction"}
@@ -129,6 +136,8 @@ def main():
     ap.add_argument("--cal-batches", type=int, default=2)
     ap.add_argument("--confidence", type=float, default=1.0 - 1e-9)
     ap.add_argument("--seed", type=int, default=2310)
+    ap.add_argument("--teacher", action=argparse.BooleanOptionalAction, default=True,
+                    help="golden set = images the model classifies like its fp32 teacher (profiler.select_golden)")
     args = ap.parse_args()
     out = run(args)
     if out is not None:

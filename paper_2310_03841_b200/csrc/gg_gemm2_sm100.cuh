@@ -369,12 +369,20 @@ __device__ __forceinline__ float tanh_approx(float x) {
   return y;
 }
 __device__ __forceinline__ float2 gelu_tanh_f32x2(float2 x) {
+  // u = x (a + b x^2), a = sqrt(2/pi), b = 0.044715 a;  gelu = x (0.5 + 0.5 tanh(u))
   const float2 x2 = mul_f32x2(x, x);
-  const float2 inner = fma_f32x2(mul_f32x2(x2, make_float2(0.044715f, 0.044715f)), x, x);  // x + 0.044715 x^3
-  const float2 u = mul_f32x2(inner, make_float2(0.7978845608028654f, 0.7978845608028654f));
+  const float2 p = fma_f32x2(x2, make_float2(0.035677408136300125f, 0.035677408136300125f),
+                             make_float2(0.7978845608028654f, 0.7978845608028654f));
+  const float2 u = mul_f32x2(x, p);
+#ifdef GG_GELU_BF16X2
+  // one MUFU for the pair: tanh.approx.bf16x2 on the packed arguments
+  uint32_t ub = pack_bf16x2(u.x, u.y), tb;
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(tb) : "r"(ub));
+  const float2 t = bf16x2_to_f32x2(tb);
+#else
   const float2 t = make_float2(tanh_approx(u.x), tanh_approx(u.y));
-  const float2 hx = mul_f32x2(x, make_float2(0.5f, 0.5f));
-  return fma_f32x2(hx, t, hx);  // 0.5 x + 0.5 x tanh(u)
+#endif
+  return mul_f32x2(x, fma_f32x2(t, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f)));
 }
 
 template <int KIND, int OUT, bool PROTECT, bool CLAIM, int ACT>

@@ -150,12 +150,13 @@ def test_calibrated_vit_flags_faults_and_replay_restores_the_clean_logits():
     del bad  # (GELU of a huge negative value is 0: this flip need not change the logits)
 
 
-def test_campaign_batched_trials_equal_single_trial_forwards():
+@pytest.mark.parametrize("modes", [("fp_exponent_bit", "fp_mantissa_bit"), ("random_value",)])
+def test_campaign_batched_trials_equal_single_trial_forwards(modes):
     """One trial per image: each image's outcome equals a forward carrying only its own fault."""
     model = ProtectedViT(SMALL, seed=6)
     model.calibrate([_images(8, SMALL, seed=s) for s in (20, 21)], confidence=1 - 1e-9)
     imgs = _images(8, SMALL, seed=22)
-    camp = ViTCampaign(model, imgs, seed=7, keep_records=True)
+    camp = ViTCampaign(model, imgs, seed=7, keep_records=True, modes=modes)
     counters = torch.zeros((SMALL.n_layers, len(FIELDS)), dtype=torch.int64, device="cuda")
     for layer in (0, 3, 5, SMALL.n_layers - 1):
         rec = camp.run_block(layer, 0, counters)
@@ -165,8 +166,9 @@ def test_campaign_batched_trials_equal_single_trial_forwards():
                 continue
             N = model.layer(layer).out_features
             r, c = i * rows + rec["element"][i] // N, rec["element"][i] % N
-            inj = K.injections_to_device([K.Injection(row=int(r), col=int(c), bit=int(rec["bit"][i]))],
-                                         torch.device("cuda"))
+            f = (K.Injection(row=int(r), col=int(c), bit=int(rec["bit"][i])) if rec["bit"][i] >= 0 else
+                 K.Injection(row=int(r), col=int(c), mode=L.GG_INJ_SET_VALUE, value=float(rec["value"][i])))
+            inj = K.injections_to_device([f], torch.device("cuda"))
             logits = model.resume(layer, camp.cache, 8, injections={layer: inj})
             mism = bool(logits[i].float().argmax() != camp.clean_pred[i])
             res = model.buffers(8).results[layer]
@@ -186,7 +188,7 @@ def test_campaign_sampler_follows_the_reference_rules():
     for layer in (1, 4, 9):
         y = camp._raw_output(layer)
         ks = np.arange(4)
-        elem, bit, mode = camp._sample(layer, ks, y)
+        elem, bit, mode, _ = camp._sample(layer, ks, y)
         lo, hi = camp.ranges[layer]
         rows = model.rows_per_image(layer)
         N = y.shape[1]
@@ -198,5 +200,5 @@ def test_campaign_sampler_follows_the_reference_rules():
             o = y[i * rows + e // N, e % N].float().item()
             assert f != o and lo <= f <= hi
         # the same (seed, layer, k) draws the same trial
-        e2, b2, _ = camp._sample(layer, ks, y)
+        e2, b2, _, _ = camp._sample(layer, ks, y)
         assert np.array_equal(elem, e2) and np.array_equal(bit, b2)
