@@ -100,7 +100,8 @@ def build_variant(name: str, defines: list[str]) -> Path:
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr[-6000:]}")
         objs.append(obj)
-    out = BUILD / f"libgemmguard_b200_{name}.so"
+    out = PKG / "_variants" / f"libgemmguard_b200_{name}.so"
+    out.parent.mkdir(exist_ok=True)
     res = subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(out), *map(str, objs), "-lcuda"],
                          capture_output=True, text=True)
     if res.returncode != 0:

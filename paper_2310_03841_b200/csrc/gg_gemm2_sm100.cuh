@@ -338,6 +338,26 @@ __device__ __forceinline__ void chk_dot(const uint4 (&v)[8], int kb, uint32_t w_
   }
 }
 
+// acc + (one 16-bit half of w) in fp32 with a single mixed-precision add (add.rn.f32.bf16 /
+// .f16: FHADD, the half selected by register aliasing); exact conversion, one rounding, so
+// the chains equal FADD over the converted values.
+template <bool BF16>
+__device__ __forceinline__ float add_f32_h16(float acc, uint32_t w, bool high) {
+  float r;
+  if (high) {
+    if constexpr (BF16)
+      asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.bf16 %0, h, %2;\n\t}" : "=f"(r) : "r"(w), "f"(acc));
+    else
+      asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.f16 %0, h, %2;\n\t}" : "=f"(r) : "r"(w), "f"(acc));
+  } else {
+    if constexpr (BF16)
+      asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.bf16 %0, l, %2;\n\t}" : "=f"(r) : "r"(w), "f"(acc));
+    else
+      asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.f16 %0, l, %2;\n\t}" : "=f"(r) : "r"(w), "f"(acc));
+  }
+  return r;
+}
+
 // Write the 32 output encodings of this thread's box row into the swizzled staging box.
 template <int OUT>
 __device__ __forceinline__ void stage_row(uint32_t box, int lane, const uint32_t (&o)[32]) {
@@ -1119,11 +1139,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               // folded into fp64 once per tile
               if (full) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {  // packed fp32 pair adds (FADD2) into two pair chains
-                  const float2 x = (OUT == O_BF16) ? bf16x2_to_f32x2(o[i])
-                                                   : __half22float2(*reinterpret_cast<const __half2*>(&o[i]));
-                  if (i & 1) obs_b = add_f32x2(obs_b, x);
-                  else obs_a = add_f32x2(obs_a, x);
+                for (int i = 0; i < 16; ++i) {  // mixed-precision adds of the 16-bit halves (FHADD: no
+                  // conversion instruction) into four fp32 chains: even pair -> a, odd pair -> b
+                  float2& acc = (i & 1) ? obs_b : obs_a;
+                  acc.x = add_f32_h16<OUT == O_BF16>(acc.x, o[i], false);
+                  acc.y = add_f32_h16<OUT == O_BF16>(acc.y, o[i], true);
                 }
               } else {
 #pragma unroll
