@@ -48,7 +48,12 @@ def reduce_counters(t: torch.Tensor) -> torch.Tensor:
         raise ValueError("campaign counters are int64 (order-independent sums)")
     r, w = world()
     if w > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        if t.is_cuda and dist.get_backend() == "gloo":  # gloo reduces host tensors
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t
 
 
