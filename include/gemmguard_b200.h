@@ -132,6 +132,13 @@ typedef struct gg_gemm_desc {
   int32_t* changed;           /* scalar: outputs whose bytes changed         */
 
   int32_t epilogue_act;       /* gg_epilogue_act (0: store the GEMM output)   */
+
+  /* Optional predicted row sums PRED[m] = sum_k A[m,k] * w_sum[k] computed by
+   * the producer of A (e.g. gg_add_layernorm's pred_out for the layer it
+   * feeds) as fp32 (hi, lo) pairs, hi in the low word; NULL: K1 forms them
+   * from its staged A tiles.  Float kinds only.  With it the kernel's
+   * checksum warps do no dot products and hold no pipeline stage. */
+  const void* pred_in;
 } gg_gemm_desc;
 
 /* Library identity. */
@@ -278,7 +285,13 @@ GG_API int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int6
  * GG_BF16, GG_F16 or GG_F32; 16-byte aligned, contiguous rows). */
 GG_API int gg_add_layernorm(int32_t dtype, const void* h, const void* y, int64_t rows, int64_t D,
                             const float* gamma, const float* beta, float eps, void* h_out,
-                            void* ln_out, void* stream);
+                            void* ln_out, const float* w_pred, uint64_t* pred_out, void* stream);
+/* If w_pred != NULL (the consumer layer's gg_checksum_aux vector, fp32 w_sum),
+ * also pred_out[row] = sum_k ln_out[row,k] * w_pred[k] over the STORED (rounded)
+ * ln_out values, as an fp32 (hi, lo) pair with lo = 0 (a per-lane fp32 FMA chain
+ * and a fixed butterfly over the warp: error <= (D/32 + 5) 2^-24 sum |x w|,
+ * inside the fused check's 2^-19 sum |terms| bound): the pred_in of the
+ * protected GEMM that consumes ln_out (guard.py:168-169's predicted side). */
 
 #ifdef __cplusplus
 }

@@ -96,6 +96,7 @@ class GGGemmDesc(ctypes.Structure):
         ("replay_rows", c_void_p),
         ("changed", c_void_p),
         ("epilogue_act", c_int32),
+        ("pred_in", c_void_p),
     ]
 
 
@@ -162,7 +163,7 @@ def load(path: Path | None = None):
                                   c_void_p]
     lib.gg_round_f64_to.restype = c_int32
     lib.gg_add_layernorm.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, ctypes.c_float,
-                                     c_void_p, c_void_p, c_void_p]
+                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     lib.gg_add_layernorm.restype = c_int32
     lib.gg_round_f64_to.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p]
     _lib = lib

@@ -211,7 +211,7 @@ class ViTCampaign:
     def _raw_output(self, i: int) -> torch.Tensor:
         """Clean raw (pre-activation) output of layer i from its cached input (unprotected launch)."""
         lin = self.model.layer(i)
-        _, x = self.cache[i]
+        x = self.cache[i][1]
         y, _ = K.protected_gemm(x, lin.weight, lin.bias, protect=False, f32_mode=lin.f32_mode, w_split=lin.w_split)
         return y
 

@@ -104,9 +104,10 @@ int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int64_t ldy
 }
 
 int gg_add_layernorm(int32_t dtype, const void* h, const void* y, int64_t rows, int64_t D, const float* gamma,
-                     const float* beta, float eps, void* h_out, void* ln_out, void* stream) {
-  return gg::launch_add_layernorm(dtype, h, y, rows, D, gamma, beta, eps, h_out, ln_out,
-                                  static_cast<cudaStream_t>(stream));
+                     const float* beta, float eps, void* h_out, void* ln_out, const float* w_pred, uint64_t* pred_out,
+                     void* stream) {
+  return gg::launch_add_layernorm(dtype, h, y, rows, D, gamma, beta, eps, h_out, ln_out, w_pred,
+                                  reinterpret_cast<unsigned long long*>(pred_out), static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

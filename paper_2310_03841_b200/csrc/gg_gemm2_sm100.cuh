@@ -456,6 +456,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
+  // predicted row sums computed here from the staged A (the checksum warps), or supplied by
+  // the producer of X (p.pred_in: e.g. the layer norm that wrote X), which frees the stages
+  const bool own_pred = PROTECT && p.pred_in == nullptr;
   const int n_tiles = p.n_tiles;
   const int m_pairs = (p.M + 2 * BM - 1) / (2 * BM);
   // The pair's tiles: a contiguous range [t0, t1) (bands folded locally) or, when the
@@ -648,7 +651,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         long long tr_empty = 0, tr_chk = 0;
 #endif
         for (int kb = 0; kb < p.k_blocks; ++kb) {
-          const bool mine = PROTECT && rem == n;
+          const bool mine = own_pred && rem == n;
           if (++rem == n_tiles) rem = 0;
 #ifdef GG_TRACE
           const long long tw0 = clock64();
@@ -705,7 +708,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #endif
         int rem = 0;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
-          const bool mine = PROTECT && rem == n;
+          const bool mine = own_pred && rem == n;
           if (++rem == n_tiles) rem = 0;
 #ifdef GG_TRACE
           const long long tf0 = clock64();
@@ -1337,8 +1340,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         // this tile's share of the band: K-blocks kb == n (mod n_tiles), software-pipelined one
         // deep so an owned stage is released as soon as it lands, not after the previous dot product
         uint4 vc[8], vn[8];
-        if (n < p.k_blocks) copy_kb(n, vn);
-        for (int kb = n; kb < p.k_blocks; kb += n_tiles) {
+        const int kb0 = own_pred ? n : p.k_blocks;  // supplied predicted sums: no dot products
+        if (kb0 < p.k_blocks) copy_kb(kb0, vn);
+        for (int kb = kb0; kb < p.k_blocks; kb += n_tiles) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) vc[j] = vn[j];
           if (kb + n_tiles < p.k_blocks) copy_kb(kb + n_tiles, vn);
@@ -1370,7 +1374,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tc_wait = tc_copy = tc_fence = tc_comp = 0;
 #endif
         unsigned long long tile_pred;  // this row's predicted partial of the tile, PRED_MODE bits
-        if constexpr (INT) tile_pred = static_cast<unsigned long long>(acci);
+        if (!own_pred) {  // the whole supplied sum enters at the band's tile 0 (folds add zeros elsewhere)
+          const long long row = static_cast<long long>(m) * 2 * BM + static_cast<long long>(rank) * BM + tid;
+          tile_pred = (n == 0 && row < p.M) ? __ldcg(static_cast<const unsigned long long*>(p.pred_in) + row) : 0ull;
+        } else if constexpr (INT) tile_pred = static_cast<unsigned long long>(acci);
         else if constexpr (PRED_PAIR)
           tile_pred = static_cast<unsigned long long>(__float_as_uint(hi)) |
                       (static_cast<unsigned long long>(__float_as_uint(lo)) << 32);

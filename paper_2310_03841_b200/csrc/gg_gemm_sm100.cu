@@ -394,6 +394,11 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.inj = d->inj;
   p.n_inj = d->n_inj;
   p.replay = replay ? 1 : 0;
+  p.pred_in = d->pred_in;
+  if (d->pred_in != nullptr) {
+    if (int_kind) return fail(GG_EUNSUPPORTED, "protected_gemm: pred_in is for float kinds (fp32 pair sums)");
+    if (reinterpret_cast<uintptr_t>(d->pred_in) & 7) return fail(GG_EINVAL, "protected_gemm: pred_in must be 8-byte aligned");
+  }
 
   p.changed = d->changed;
   if (protect) {

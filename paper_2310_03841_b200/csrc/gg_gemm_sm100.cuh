@@ -72,6 +72,7 @@ struct Params {
                         // exchanges, 256 finisher folds without finishing, 8192 no
                         // launch-summary atomics,
                         // 1024 / 2048 force the contiguous / strided schedule
+  const void* pred_in;  // [M] predicted row sums (fp32 (hi, lo) pairs) supplied by X's producer, or null
   int replay;           // 1: only active bands, compare against old C
   int* changed;
   Workspace ws;

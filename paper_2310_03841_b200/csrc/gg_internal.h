@@ -66,7 +66,8 @@ int launch_int_finish(const int* y, int64_t B, int64_t T, int64_t N, int64_t ldy
 
 // implemented in gg_vit.cu
 int launch_add_layernorm(int dtype, const void* h, const void* y, int64_t rows, int64_t D, const float* gamma,
-                         const float* beta, float eps, void* h_out, void* ln_out, cudaStream_t s);
+                         const float* beta, float eps, void* h_out, void* ln_out, const float* w_pred,
+                         unsigned long long* pred_out, cudaStream_t s);
 
 // implemented in gg_gemm_sm100.cu
 size_t protected_gemm_workspace_bytes(int64_t M, int64_t N);

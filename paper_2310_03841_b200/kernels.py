@@ -154,6 +154,7 @@ def build_desc(
     replay_rows: torch.Tensor | None = None,
     changed: torch.Tensor | None = None,
     act: int = L.GG_ACT_NONE,
+    pred_in: torch.Tensor | None = None,
 ) -> L.GGGemmDesc:
     M, K = x.shape
     N = w.shape[0]
@@ -188,6 +189,7 @@ def build_desc(
     d.replay_rows = _ptr(replay_rows)
     d.changed = _ptr(changed)
     d.epilogue_act = int(act)
+    d.pred_in = _ptr(pred_in) if protect else None
     return d
 
 
@@ -262,6 +264,12 @@ def default_out_dtype(ab: torch.dtype) -> torch.dtype:
             torch.int8: torch.int32}[ab]
 
 
+def _check_pred(pred_in: torch.Tensor | None, M: int) -> torch.Tensor | None:
+    if pred_in is not None and (pred_in.dtype != torch.int64 or pred_in.numel() < M or not pred_in.is_contiguous()):
+        raise ValueError("pred_in must be a contiguous int64 (fp32 pair bits) tensor with one entry per row")
+    return pred_in
+
+
 def _prepare_operands(x, w, w_sum, w_aux, protect, f32_mode, w_split):
     """TMA-ready operands (16-byte pitches) and the matching checksum encoding;
     fp32 operands are expanded for 3xTF32 unless f32_mode="tf32"."""
@@ -304,6 +312,7 @@ def protected_gemm(
     f32_mode: str = "3xtf32",
     w_split: torch.Tensor | None = None,
     act: int = L.GG_ACT_NONE,
+    pred_in: torch.Tensor | None = None,
 ) -> tuple[torch.Tensor, CheckResult | None]:
     """K1: y = x @ w.T + bias with the fused checksum check (one launch).
 
@@ -311,6 +320,8 @@ def protected_gemm(
     fp32 operands run as 3xTF32 (binary32 accuracy; `w_split` may hold the
     weight's cached `split_tf32x3(w, 1)`) unless f32_mode="tf32" (one tf32 pass).
     act=GG_ACT_GELU_TANH stores GELU(y) (16-bit outputs) after the check of y.
+    pred_in [M] (uint64 fp32 (hi, lo) pairs): the predicted row sums x . w_sum
+    computed by x's producer (add_layernorm's pred_out); K1 then skips its own.
     Returns (y, CheckResult or None when protect=False).
     """
     dev = _require_cuda(x, w, bias)
@@ -333,7 +344,8 @@ def protected_gemm(
     else:
         inj_dev, n_inj = None, 0
     desc = build_desc(x, w, y, bias, protect=protect, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo,
-                      hi=hi, statistic=statistic, result=result, inj_dev=inj_dev, n_inj=n_inj, ws=ws, act=act)
+                      hi=hi, statistic=statistic, result=result, inj_dev=inj_dev, n_inj=n_inj, ws=ws, act=act,
+                      pred_in=_check_pred(pred_in, M))
     L.check(L.load().gg_protected_gemm(ctypes.byref(desc), _stream(dev)), "gg_protected_gemm")
     return y, (result if protect else None)
 
@@ -405,6 +417,7 @@ def replay_tiles(
     f32_mode: str = "3xtf32",
     w_split: torch.Tensor | None = None,
     act: int = L.GG_ACT_NONE,
+    pred_in: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """K4: recompute only the M-bands holding a flagged row, in place in y.
 
@@ -419,7 +432,8 @@ def replay_tiles(
     changed = changed if changed is not None else torch.zeros(1, dtype=torch.int32, device=dev)
     ws = workspace(M, N, dev, ws_key)
     desc = build_desc(x, w, y, bias, protect=True, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
-                      statistic=statistic, result=result, ws=ws, replay_rows=replay_rows, changed=changed, act=act)
+                      statistic=statistic, result=result, ws=ws, replay_rows=replay_rows, changed=changed, act=act,
+                      pred_in=_check_pred(pred_in, M))
     L.check(L.load().gg_replay_tiles(ctypes.byref(desc), _stream(dev)), "gg_replay_tiles")
     return changed
 
@@ -525,13 +539,19 @@ def reduce(a: torch.Tensor, axis: int) -> torch.Tensor:
 
 
 def add_layernorm(h: torch.Tensor, y: torch.Tensor | None, gamma: torch.Tensor, beta: torch.Tensor, eps: float,
-                  ln_out: torch.Tensor, h_out: torch.Tensor | None = None) -> None:
-    """gg_add_layernorm: h_out = h + y (if y is given; h_out may be h), ln_out = LN(.) * gamma + beta."""
+                  ln_out: torch.Tensor, h_out: torch.Tensor | None = None, w_pred: torch.Tensor | None = None,
+                  pred_out: torch.Tensor | None = None) -> None:
+    """gg_add_layernorm: h_out = h + y (if y is given; h_out may be h), ln_out = LN(.) * gamma + beta,
+    and with w_pred (the consumer's fp32 checksum_aux) pred_out[row] = ln_out[row] . w_pred as
+    fp32 (hi, lo) pair bits (the consumer launch's pred_in)."""
     dev = _require_cuda(h, y, gamma, beta, ln_out, h_out)
     rows, D = h.shape
     for t in (h, y, ln_out, h_out):
         if t is not None and (not t.is_contiguous() or t.shape != (rows, D) or t.dtype != h.dtype):
             raise ValueError("add_layernorm takes contiguous [rows, D] tensors of one dtype")
+    if w_pred is not None and (w_pred.dtype != torch.uint8 and w_pred.dtype != torch.float32):
+        raise ValueError("w_pred is the consumer's fp32 checksum_aux vector")
     L.check(L.load().gg_add_layernorm(TORCH_TO_GG[h.dtype], h.data_ptr(), _ptr(y), rows, D, gamma.data_ptr(),
-                                      beta.data_ptr(), float(eps), _ptr(h_out), ln_out.data_ptr(), _stream(dev)),
+                                      beta.data_ptr(), float(eps), _ptr(h_out), ln_out.data_ptr(), _ptr(w_pred),
+                                      _ptr(pred_out), _stream(dev)),
             "gg_add_layernorm")

@@ -154,19 +154,30 @@ class ProtectedLinear(torch.nn.Module):
         return kw
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, result: K.CheckResult | None = None,
-                injections: torch.Tensor | None = None, protect: bool | None = None) -> torch.Tensor:
+                injections: torch.Tensor | None = None, protect: bool | None = None,
+                pred_in: torch.Tensor | None = None) -> torch.Tensor:
+        """pred_in: x . w_sum computed by x's producer (kernels.add_layernorm with w_pred=self.aux)."""
         p = self.protected if protect is None else protect
         y, res = K.protected_gemm(x, self.weight, self.bias, out=out, result=result, injections=injections,
-                                  **self._kw(p))
+                                  pred_in=pred_in if p else None, **self._kw(p))
         self.result = res
+        self.last_pred_in = pred_in if p else None
         return y
+
+    @property
+    def pred_vector(self) -> torch.Tensor | None:
+        """fp32 w_sum for a producer-side predicted sum (16-bit and single-pass tf32 kinds)."""
+        if self.integer or (self.weight.dtype == torch.float32 and self.f32_mode == "3xtf32"):
+            return None
+        return self.aux
 
     def replay(self, x: torch.Tensor, y: torch.Tensor, rows: torch.Tensor, result: K.CheckResult,
                changed: torch.Tensor | None = None) -> torch.Tensor:
         """K4 on this layer's last launch: recompute the bands of the flagged rows in place."""
         kw = self._kw(True)
         kw.pop("protect")
-        return K.replay_tiles(x, self.weight, self.bias, y, rows, result, changed=changed, **kw)
+        return K.replay_tiles(x, self.weight, self.bias, y, rows, result, changed=changed,
+                              pred_in=getattr(self, "last_pred_in", None), **kw)
 
 
 @dataclass
@@ -182,6 +193,7 @@ class _Buffers:
     f: torch.Tensor
     cls_in: torch.Tensor
     logits: torch.Tensor
+    pred: torch.Tensor | None = None  # [B*T] predicted sums of the next GEMM, from the layer norm
     results: dict = field(default_factory=dict)
     o_view: torch.Tensor | None = None  # the proj input: the attention output itself when contiguous, else o
 
@@ -217,6 +229,10 @@ class ProtectedViT(torch.nn.Module):
         self.register_buffer("ln_b", 0.02 * torch.randn(n_ln, D, device=dev, generator=g))
         self._bufs: dict[int, _Buffers] = {}
         self.hooks = []  # callables (layer, result) after every protected launch (calibration)
+        # Optionally the layer norms that feed qkv / fc1 also form those launches' predicted row
+        # sums (pred_in), so K1's checksum warps hold no pipeline stage there.  Measured on ViT-B
+        # b256: K1 qkv / fc1 -6 / -8 us per launch, the layer norm +9 us: a wash, so off by default.
+        self.producer_pred = False
 
     # ------------------------------------------------------------- plumbing
     def layer(self, i: int) -> ProtectedLinear:
@@ -238,7 +254,8 @@ class ProtectedViT(torch.nn.Module):
             bf = _Buffers(B=B, patches=e(B * (T - 1), c.patch_dim), e=e(B * (T - 1), D), h=e(B * T, D),
                           a=e(B * T, D), qkv=e(B * T, 3 * D), o=e(B * T, D), y=e(B * T, D), f=e(B * T, c.mlp),
                           cls_in=e(B, D), logits=torch.empty(B, c.classes, device=dev,
-                                                             dtype=torch.int32 if dt == torch.int8 else dt))
+                                                             dtype=torch.int32 if dt == torch.int8 else dt),
+                          pred=torch.empty(B * T, device=dev, dtype=torch.int64))
             for lin in self.linears:
                 M = B * self.rows_per_image(lin.index)
                 bf.results[lin.index] = K.CheckResult.empty(M, lin.integer, dev)
@@ -251,12 +268,27 @@ class ProtectedViT(torch.nn.Module):
         for lin in self.linears:
             lin.protected = lin.index in chosen
 
+    def _feeds_pred(self, i: int, protect) -> bool:
+        """Whether the layer norm writing layer i's input also forms its predicted sums."""
+        lin = self.linears[i]
+        on = lin.protected if protect is None else (protect and lin.protected)
+        return bool(self.producer_pred and on and lin.pred_vector is not None)
+
+    def _ln_into(self, i: int, protect, bf: _Buffers, h, y, g, b, h_out=None) -> None:
+        """a = LN(h [+ y]) feeding protected layer i (with its pred_in when enabled)."""
+        feeds = self._feeds_pred(i, protect)
+        K.add_layernorm(h, y, g, b, self.cfg.ln_eps, ln_out=bf.a, h_out=h_out,
+                        w_pred=self.linears[i].pred_vector if feeds else None, pred_out=bf.pred if feeds else None)
+        bf.pred_valid = feeds
+
     def _lin(self, i: int, x: torch.Tensor, out: torch.Tensor, bf: _Buffers, protect: bool | None,
-             injections: dict | None) -> torch.Tensor:
+             injections: dict | None, pred: bool = False) -> torch.Tensor:
         lin = self.linears[i]
         inj = injections.get(i) if injections else None
+        use_pred = pred and getattr(bf, "pred_valid", False) and self._feeds_pred(i, protect)
         y = lin(x, out=out, result=bf.results[i], injections=inj,
-                protect=None if protect is None else (protect and lin.protected))
+                protect=None if protect is None else (protect and lin.protected),
+                pred_in=bf.pred if use_pred else None)
         if lin.result is not None:
             for h in self.hooks:
                 h(lin, lin.result)
@@ -306,13 +338,17 @@ class ProtectedViT(torch.nn.Module):
 
         def save(i, resid, x):
             if cache is not None:
-                cache[i] = (None if resid is None else resid.clone(), x.clone())
+                pv = bf.pred.clone() if getattr(bf, "pred_valid", False) and x is a else None
+                cache[i] = (None if resid is None else resid.clone(), x.clone(), pv)
 
         def load(i, resid, x):
-            r, xi = restore[i]
+            r, xi, pv = restore[i]
             if r is not None:
                 resid.copy_(r)
             x.copy_(xi)
+            bf.pred_valid = pv is not None
+            if pv is not None:
+                bf.pred.copy_(pv)
 
         if start == 0:
             save(0, None, bf.patches)
@@ -320,14 +356,14 @@ class ProtectedViT(torch.nn.Module):
             hv = h.view(B, T, D)
             torch.add(bf.e.view(B, T - 1, D), self.pos[1:], out=hv[:, 1:])
             hv[:, 0] = self.cls + self.pos[0]
-            K.add_layernorm(h, None, *self._ln(0), eps, ln_out=a)
+            self._ln_into(1, protect, bf, h, None, *self._ln(0))
         for b in range(c.depth):
             base = 1 + 4 * b
             if start <= base:
                 if start == base:
                     load(base, h, a)
                 save(base, h, a)
-                self._lin(base, a, bf.qkv, bf, protect, inj)
+                self._lin(base, a, bf.qkv, bf, protect, inj, pred=True)
                 self._attention(bf)
             if start <= base + 1:
                 if start == base + 1:
@@ -335,12 +371,12 @@ class ProtectedViT(torch.nn.Module):
                     bf.o_view = bf.o
                 save(base + 1, h, bf.o_view)
                 self._lin(base + 1, bf.o_view, bf.y, bf, protect, inj)
-                K.add_layernorm(h, bf.y, *self._ln(2 * b + 1), eps, ln_out=a, h_out=h)
+                self._ln_into(base + 2, protect, bf, h, bf.y, *self._ln(2 * b + 1), h_out=h)
             if start <= base + 2:
                 if start == base + 2:
                     load(base + 2, h, a)
                 save(base + 2, h, a)
-                self._lin(base + 2, a, bf.f, bf, protect, inj)
+                self._lin(base + 2, a, bf.f, bf, protect, inj, pred=True)
                 if not self.fused_gelu:
                     bf.f.copy_(F.gelu(bf.f, approximate="tanh"))
             if start <= base + 3:
@@ -348,7 +384,12 @@ class ProtectedViT(torch.nn.Module):
                     load(base + 3, h, bf.f)
                 save(base + 3, h, bf.f)
                 self._lin(base + 3, bf.f, bf.y, bf, protect, inj)
-                K.add_layernorm(h, bf.y, *self._ln(2 * b + 2), eps, ln_out=a, h_out=h)
+                nxt = base + 4 if b + 1 < c.depth else None  # the next qkv (the final norm feeds the head's cls rows)
+                if nxt is not None:
+                    self._ln_into(nxt, protect, bf, h, bf.y, *self._ln(2 * b + 2), h_out=h)
+                else:
+                    K.add_layernorm(h, bf.y, *self._ln(2 * b + 2), eps, ln_out=a, h_out=h)
+                    bf.pred_valid = False
         head = c.n_layers - 1
         if start == head:
             load(head, None, bf.cls_in)

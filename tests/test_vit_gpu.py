@@ -202,3 +202,24 @@ def test_campaign_sampler_follows_the_reference_rules():
         # the same (seed, layer, k) draws the same trial
         e2, b2, _, _ = camp._sample(layer, ks, y)
         assert np.array_equal(elem, e2) and np.array_equal(bit, b2)
+
+
+def test_layernorm_supplied_predicted_sums_match_the_kernels_own():
+    """pred_in from gg_add_layernorm (over the stored LN output) gives the same d as K1's own
+    predicted side within the fused-d bound, and the same flags at a calibrated epsilon."""
+    model = ProtectedViT(SMALL, seed=9)
+    cal = [_images(8, SMALL, seed=s) for s in (40, 41)]
+    model.calibrate(cal, confidence=0.9999)
+    imgs = _images(8, SMALL, seed=42)
+    ds = {}
+    for flag in (True, False):
+        model.producer_pred = flag  # off by default (DESIGN.md: a wash on ViT-B), must stay correct
+        logits = model(imgs).clone()
+        ds[flag] = ({i: model.buffers(8).results[i].d.clone() for i in range(SMALL.n_layers)},
+                    {i: model.buffers(8).results[i].flags.clone() for i in range(SMALL.n_layers)}, logits)
+    assert torch.equal(ds[True][2], ds[False][2])  # the GEMM outputs do not depend on it
+    for i in range(SMALL.n_layers):
+        a, b = ds[True][0][i], ds[False][0][i]
+        scale = a.abs().max().item() + 1.0
+        assert float((a - b).abs().max()) <= 2.0**-16 * scale * SMALL.mlp, i
+        assert torch.equal(ds[True][1][i], ds[False][1][i]), i

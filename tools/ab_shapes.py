@@ -12,16 +12,18 @@ for name, M, N, Kd, act in shapes:
     b = torch.zeros(N, device='cuda'); ws, bs = K.offline_checksum(w, b, L.GG_P_F64); bsv = bs.item()
     aux = K.checksum_aux(ws, torch.bfloat16); y = torch.empty(M, N, device='cuda', dtype=torch.bfloat16)
     res = K.CheckResult.empty(M, False, 'cuda')
+    pred = torch.zeros(M, dtype=torch.int64, device='cuda')
     def run(prot):
-        if prot: K.protected_gemm(x, w, b, w_sum=ws, w_aux=aux, bias_sum=bsv, lo=-1e30, hi=1e30, act=act, out=y, result=res)
+        if prot: K.protected_gemm(x, w, b, w_sum=ws, w_aux=aux, bias_sum=bsv, lo=-1e30, hi=1e30, act=act, out=y, result=res,
+                                  pred_in=pred if prot == 2 else None)
         else: K.protected_gemm(x, w, b, protect=False, act=act, out=y)
-    t = {0: [], 1: []}
+    t = {0: [], 1: [], 2: []}
     for it in range(30):
-        for prot in ((0, 1) if it % 2 else (1, 0)):
+        for prot in ((0, 1, 2) if it % 2 else (2, 1, 0)):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(); run(prot); e1.record(); torch.cuda.synchronize()
             if it >= 4: t[prot].append(e0.elapsed_time(e1) * 1e3)
-    u, p = statistics.median(t[0]), statistics.median(t[1])
-    rows.append(f"{name:9s} unprot {u:7.1f} us  prot {p:7.1f} us  overhead {100*(p/u-1):5.1f}%")
+    u, p, q = statistics.median(t[0]), statistics.median(t[1]), statistics.median(t[2])
+    rows.append(f"{name:9s} unprot {u:7.1f} us  prot {p:7.1f} us  overhead {100*(p/u-1):5.1f}%  | with pred_in {q:7.1f} us {100*(q/u-1):5.1f}%")
 print(os.environ.get('GEMMGUARD_LIB', 'default').split('/')[-1]); print("\n".join(rows))

@@ -1,16 +1,18 @@
-"""add_layernorm on a ViT-B b256 residual stream, for ncu."""
+"""add_layernorm on a ViT-B b256 residual stream, with and without the consumer's predicted sums."""
 import sys, torch
 sys.path.insert(0, '.')
 from paper_2310_03841_b200 import kernels as K
 h = torch.randn(50432, 768, device='cuda').bfloat16(); y = torch.randn_like(h); ln = torch.empty_like(h)
 g = torch.ones(768, device='cuda'); b = torch.zeros(768, device='cuda')
-for _ in range(3):
-    K.add_layernorm(h, y, g, b, 1e-6, ln_out=ln, h_out=h)
-torch.cuda.synchronize()
-t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-t0.record()
-for _ in range(20):
-    K.add_layernorm(h, y, g, b, 1e-6, ln_out=ln, h_out=h)
-t1.record(); torch.cuda.synchronize()
-us = t0.elapsed_time(t1) / 20 * 1e3
-print(f"add_layernorm 50432x768 bf16: {us:.1f} us, {4 * h.numel() * 2 / us / 1e3:.0f} GB/s")
+w = torch.randn(768, device='cuda'); pred = torch.empty(50432, dtype=torch.int64, device='cuda')
+for label, kw in (("plain", {}), ("with pred", dict(w_pred=w, pred_out=pred))):
+    for _ in range(3):
+        K.add_layernorm(h, y, g, b, 1e-6, ln_out=ln, h_out=h, **kw)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(20):
+        K.add_layernorm(h, y, g, b, 1e-6, ln_out=ln, h_out=h, **kw)
+    t1.record(); torch.cuda.synchronize()
+    us = t0.elapsed_time(t1) / 20 * 1e3
+    print(f"add_layernorm 50432x768 bf16 {label}: {us:.1f} us, {4 * h.numel() * 2 / us / 1e3:.0f} GB/s")
