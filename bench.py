@@ -515,6 +515,7 @@ def main():
     import torch
 
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr: one rank per GPU, NVLink paths
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_ours(args, rank, world, local_rank)
