@@ -406,8 +406,10 @@ def coverage_study(model, held, images, args, rank, world, dev) -> dict:
     del teacher
     torch.cuda.empty_cache()
 
+    from paper_2310_03841_b200.campaign_vit import calibrate_distributed
+
     def one(m, imgs, c, cal, tag, modes=("fp_exponent_bit", "fp_mantissa_bit")):
-        m.calibrate(cal, c)
+        calibrate_distributed(m, cal, c)  # every rank's batches, moments merged in rank order
         t0 = time.perf_counter()
         camp = ViTCampaign(m, imgs, seed=2310, modes=modes)
         tally = camp.run(args.campaign_blocks, rank=rank, world_size=world)
