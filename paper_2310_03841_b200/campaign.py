@@ -52,7 +52,11 @@ __all__ = ["ViTCampaign", "CampaignTally", "wilson_interval", "plan_units", "sel
            "BF16_FIELDS"]
 
 FIELDS = ("injections", "mismatches", "true_positives", "false_negatives", "benign_detections", "true_negatives",
-          "skipped")
+          "skipped", "loss_delta_fx")
+# loss shifts are summed as int64 fixed point (2^-32 units) so that K5's all-reduce stays an
+# order-independent integer sum; a non-finite or huge shift counts as +/-LOSS_CLAMP
+LOSS_FX = 2.0**32
+LOSS_CLAMP = 1.0e6
 # (mantissa, exponent) bits per device dtype; bfloat16 is an extension (the reference has no bf16 tag)
 BF16_FIELDS = {torch.bfloat16: (7, 8), torch.float16: (10, 5), torch.float32: (23, 8)}
 MAX_RETRIES = 64  # injector.py:53
@@ -98,6 +102,14 @@ class CampaignTally:
 
     def total(self, name: str) -> int:
         return int(self.counters[:, FIELDS.index(name)].sum())
+
+    def layer(self, i: int) -> dict:
+        """Tallies of one layer, with the mean loss shift (corrupted - clean; injector.py:335-345)."""
+        row = {name: int(v) for name, v in zip(FIELDS, self.counters[i])}
+        n = row["injections"]
+        row["loss_delta_sum"] = row.pop("loss_delta_fx") / LOSS_FX
+        row["delta_loss"] = row["loss_delta_sum"] / n if n else 0.0
+        return row
 
     @property
     def coverage(self) -> float:
@@ -189,6 +201,7 @@ class ViTCampaign:
         with torch.no_grad():
             logits = model.forward(images, protect=True, cache=self.cache)
             self.clean_pred = logits.float().argmax(dim=1).clone()
+            self.clean_loss = torch.nn.functional.cross_entropy(logits.float(), self.clean_pred, reduction="none")
             self.clean_flags = {i: self._image_flags(i) for i in range(model.cfg.n_layers)}
             res = model.buffers(self.G).results
             self._clean_nflag = dict(enumerate(torch.cat([res[i].nflag for i in range(model.cfg.n_layers)])
@@ -303,14 +316,19 @@ class ViTCampaign:
                for r, c, b, v, o in zip(grow, gcol, bit, value, ok) if o]
         inj_dev = K.injections_to_device(inj, self.dev)
         logits = self.model.resume(layer, self.cache, G, protect=True, injections={layer: inj_dev})
-        pred = logits.float().argmax(dim=1)
+        lg = logits.float()
+        pred = lg.argmax(dim=1)
+        # loss shift against the clean prediction as label (the golden label, profiler.py:83-96)
+        loss = torch.nn.functional.cross_entropy(lg, self.clean_pred, reduction="none")
+        dl = torch.nan_to_num(loss - self.clean_loss, nan=LOSS_CLAMP, posinf=LOSS_CLAMP, neginf=-LOSS_CLAMP)
+        dl_fx = torch.round(dl.clamp(-LOSS_CLAMP, LOSS_CLAMP).double() * LOSS_FX).to(torch.int64)
         okd = torch.from_numpy(ok).to(self.dev)
         mism = (pred != self.clean_pred) & okd
         det = self._image_flags(layer) & okd
         if not self.model.layer(layer).protected:
             det = torch.zeros_like(det)
         row = torch.stack([okd.sum(), mism.sum(), (mism & det).sum(), (mism & ~det).sum(), (~mism & det & okd).sum(),
-                           (~mism & ~det & okd).sum(), (~okd).sum()]).to(torch.int64)
+                           (~mism & ~det & okd).sum(), (~okd).sum(), torch.where(okd, dl_fx, 0).sum()]).to(torch.int64)
         counters[layer] += row
         if not self.keep_records:
             return None

@@ -176,7 +176,7 @@ def test_campaign_batched_trials_equal_single_trial_forwards(modes):
             assert mism == bool(rec["mismatch"][i]) and det == bool(rec["detected"][i]), (layer, i)
     c = counters.cpu().numpy()
     for layer in (0, 3, 5, SMALL.n_layers - 1):
-        inj, mm, tp, fn, ben, tn, sk = c[layer]
+        inj, mm, tp, fn, ben, tn, sk, _loss = c[layer]
         assert inj + sk == 8 and tp + fn == mm and tp + fn + ben + tn == inj
 
 
