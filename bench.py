@@ -58,8 +58,8 @@ D, MLP, BLOCKS, CLASSES = 768, 3072, 12, 1000
 CONFIDENCE = 1.0 - 1e-9  # per-row checks: ~50k rows x 50 layers per step => keep false flags << 1 per step
 
 # DRAM bytes (read + write) per protected launch, from `ncu --set full` captures of K1
-# (profiles/r01/ncu_full_bf16_vitb.json; profiles/ does not travel to the box)
-NCU_DRAM_MB = {"qkv": 282.1, "proj": 116.5, "fc1": 371.7, "fc2": 382.4}
+# (profiles/r02/full_{proj,fc2}.ncu-rep and SUMMARY.md; profiles/ does not travel to the box)
+NCU_DRAM_MB = {"qkv": 282.7, "proj": 115.5, "fc1": 368.5, "fc2": 383.8}
 
 
 def step_traffic_bytes() -> float:
