@@ -85,7 +85,7 @@ def run(args) -> dict | None:
         torch.cuda.empty_cache()
     else:
         golden = mk(gold_g)
-    camp = ViTCampaign(model, golden, seed=args.seed)
+    camp = ViTCampaign(model, golden, seed=args.seed, modes=tuple(args.modes.split(",")))
     n_layers = cfg.n_layers
     per_layer = math.ceil(args.trials / n_layers)
     n_blocks = math.ceil(per_layer / args.batch)
@@ -121,7 +121,7 @@ def run(args) -> dict | None:
             "skipped": summ["skipped"], "blocks_per_layer": n_blocks, "images_per_block": args.batch,
             "device_s": s, "wall_s": wall, "trials_per_s": summ["injections"] / s,
             "full_forward_flop_per_trial": gemm_f + attn_f, "confidence": args.confidence,
-            "summary": summ, "by_role": roles, "golden": gstats,
+            "summary": summ, "by_role": roles, "golden": gstats, "modes": args.modes,
             "scope": "one output bit flip per image of a 256-image batch at one protected layer, prefix reuse "
                      "(forward resumed at the layer), range-constrained exponent/mantissa flips, mismatch = "
                      "argmax change vs the clean prediction"}
@@ -136,6 +136,8 @@ def main():
     ap.add_argument("--cal-batches", type=int, default=2)
     ap.add_argument("--confidence", type=float, default=1.0 - 1e-9)
     ap.add_argument("--seed", type=int, default=2310)
+    ap.add_argument("--modes", default="fp_exponent_bit,fp_mantissa_bit",
+                    help="comma-separated sample_injection modes (bit modes or random_value)")
     ap.add_argument("--teacher", action=argparse.BooleanOptionalAction, default=True,
                     help="golden set = images the model classifies like its fp32 teacher (profiler.select_golden)")
     args = ap.parse_args()
