@@ -408,6 +408,9 @@ def run_campaign(model: ModelGraph, golden: GoldenSet, ranges: RangeProfile, n_p
     if n_per_layer == 0:
         return CampaignResult(records=[], seed=seed, n_per_layer=0, skipped={})
     mine = [li for li in range(len(model.layers)) if li % world == rank]
+    if model.is_integer and tuple(locations) == ("output",):
+        return _assemble(_batched_layer_campaigns(model, golden, ranges, mine, n_per_layer, modes, seed), seed,
+                         n_per_layer)
     args = [(model, golden, ranges, li, range(n_per_layer), modes, locations, seed) for li in mine]
     if workers > 1:
         with ProcessPoolExecutor(max_workers=workers, mp_context=multiprocessing.get_context("spawn")) as pool:
@@ -415,6 +418,30 @@ def run_campaign(model: ModelGraph, golden: GoldenSet, ranges: RangeProfile, n_p
     else:
         results = [_layer_campaign(*a) for a in args]
     return _assemble(results, seed, n_per_layer)
+
+
+def _batched_layer_campaigns(model, golden, ranges, layers, n_per_layer, modes, seed):
+    """Integer models, output faults: each layer's trials run as batched device forwards
+    (guard.batched_injected_forwards, one fault per image in its own rows), drawn from the
+    same per-trial streams as `_layer_campaign`; the records are identical."""
+    from .guard import batched_injected_forwards, draw_trials
+
+    tag = output_dtype(model)
+    results, traces = [], {}
+    for li in layers:
+        drawn, traces = draw_trials(model, golden, ranges, li, range(n_per_layer), modes, seed, traces=traces)
+        trials = [t for t in drawn if t[2] is not None]
+        outs = batched_injected_forwards(model, golden, li, trials, protect=False)
+        recs = []
+        for (k, sid, spec), (_, pred, loss, _, _) in zip(trials, outs):
+            clean = traces[sid]
+            orig = _scalar(clean.outputs[li].widened().ravel()[spec.element_index], tag)
+            recs.append(InjectionRecord(spec=spec, original_value=orig, corrupted_value=corrupted_value_for(spec, orig, tag),
+                                        golden_loss=clean.loss, corrupted_loss=loss,
+                                        golden_class=clean.predicted_class, corrupted_class=pred,
+                                        mismatch=pred != clean.predicted_class))
+        results.append((li, recs, len(drawn) - len(trials)))
+    return results
 
 
 def _assemble(results, seed: int, n_per_layer: int) -> CampaignResult:

@@ -42,6 +42,15 @@ class BatchForward:
     predicted: np.ndarray  # [B] int
     losses: np.ndarray | None  # [B] softmax cross-entropy when labels are given
     flagged: dict[int, np.ndarray] | None  # protect=True: layer -> [B] bool (any flagged row of the sample)
+    flagged_rows: dict[int, np.ndarray] | None = None  # protect=True: layer -> [B] flagged rows of the sample
+    max_disc: dict[int, np.ndarray] | None = None  # protect=True: layer -> [B] max |d| over the sample's rows
+
+
+def output_injection(spec_mode: str, bit, value, row: int, col: int) -> K.Injection:
+    """An output fault of sample_injection as an in-epilogue descriptor (bit flip or value)."""
+    if bit is not None and spec_mode not in ("random_value", "fixed_value"):
+        return K.Injection(row=row, col=col, bit=int(bit))
+    return K.Injection(row=row, col=col, mode=L.GG_INJ_SET_VALUE, value=float(value))
 
 
 _CHK: dict[int, tuple[torch.Tensor, int]] = {}  # id(weight Matrix2D) -> (w_sum, bias_sum), dropped with the weight
@@ -61,7 +70,10 @@ def _checksum(layer, w_nk: torch.Tensor, bias: torch.Tensor):
 
 def forward_batch(model: ModelGraph, inputs: Sequence[Matrix2D], labels: Sequence[int] | None = None, *,
                   protect: bool = False, ranges: dict[int, RunningRange] | None = None,
-                  device: torch.device | str = "cuda") -> BatchForward:
+                  device: torch.device | str = "cuda", injections: dict | None = None,
+                  chks: dict | None = None) -> BatchForward:
+    """Batched integer forward.  `injections`: {layer: [K.Injection]} output faults applied in
+    that layer's GEMM epilogue (rows of the batched output: sample * rows_per_sample + row)."""
     if not model.is_integer:
         raise NotImplementedError("device glue covers integer models; float models use model.forward")
     if len(inputs) == 0:
@@ -76,19 +88,27 @@ def forward_batch(model: ModelGraph, inputs: Sequence[Matrix2D], labels: Sequenc
     lib = L.load()
     stream = torch.cuda.current_stream(dev).cuda_stream
     flags = {} if protect else None
+    nrows = {} if protect else None
+    maxd = {} if protect else None
     logits = None
     for layer in model.layers:
         ent = device_layer(layer, model.dtype, "tensor")
         bias = ent.bias[("tensor", id(layer.bias))]
         head = layer.kind == "head"
         xin = h.view(B, T, -1)[:, 0, :].contiguous() if head else h
+        inj = injections.get(layer.index) if injections else None
         if protect:
-            ws, bs = _checksum(layer, ent.w_nk, bias)
-            y, res = K.protected_gemm(xin, ent.w_nk, bias, w_sum=ws, bias_sum=bs, lo=0, hi=0)
+            if chks is not None and layer.index in chks:  # the caller's offline checksums (guard.WeightChecksum)
+                ws, bs = chks[layer.index].w_sum_device(), int(chks[layer.index].bias_sum)
+            else:
+                ws, bs = _checksum(layer, ent.w_nk, bias)
+            y, res = K.protected_gemm(xin, ent.w_nk, bias, w_sum=ws, bias_sum=bs, lo=0, hi=0, injections=inj)
             rows = res.flags.view(B, -1) if not head else res.flags.view(B, 1)
-            flags[layer.index] = rows.any(dim=1)
+            flags[layer.index] = rows.bool().any(dim=1)
+            nrows[layer.index] = rows.to(torch.int32).sum(dim=1)
+            maxd[layer.index] = res.d.view(B, -1).abs().max(dim=1).values
         else:
-            y, _ = K.protected_gemm(xin, ent.w_nk, bias, protect=False)
+            y, _ = K.protected_gemm(xin, ent.w_nk, bias, protect=False, injections=inj)
         if ranges is not None:
             ranges.setdefault(layer.index, RunningRange(dev)).update(y)
         if head:
@@ -104,4 +124,6 @@ def forward_batch(model: ModelGraph, inputs: Sequence[Matrix2D], labels: Sequenc
     pred = lg.argmax(axis=1)
     losses = None if labels is None else np.array([loss_from_logits(lg[i], int(labels[i])) for i in range(B)])
     fl = None if flags is None else {i: f.cpu().numpy() for i, f in flags.items()}
-    return BatchForward(logits=lg, predicted=pred, losses=losses, flagged=fl)
+    nr = None if nrows is None else {i: f.cpu().numpy() for i, f in nrows.items()}
+    md = None if maxd is None else {i: f.cpu().numpy() for i, f in maxd.items()}
+    return BatchForward(logits=lg, predicted=pred, losses=losses, flagged=fl, flagged_rows=nr, max_disc=md)
