@@ -298,12 +298,19 @@ def gemm_only(args, dev, world, stream):
     gp = _capture(lambda: [launch(ly, True) for ly in layers])
     gu = _capture(lambda: [launch(ly, False) for ly in layers])
     ms_p, ms_u = _interleaved(gp.replay, gu.replay, 6, max(3, args.steps // 2), args.warmup, world, dev, stream)
+    # the library baseline: the same 50 GEMMs (+ bias) through cuBLAS, unprotected
+    for ly in layers:
+        ly["bb"] = ly["b"].to(torch.bfloat16)
+    gc = _capture(lambda: [torch.addmm(ly["bb"], ly["x"], ly["w"].t(), out=ly["y"]) for ly in layers])
+    ms_c = _timed(gc.replay, max(3, args.steps // 2), args.warmup, world, dev, stream)
     flops = gemm_flops(gemms)
     out = {"protected_gemm_tflops": flops / (ms_p * 1e-3) / 1e12, "unprotected_gemm_tflops": flops / (ms_u * 1e-3) / 1e12,
            "gemm_overhead_pct": 100.0 * (ms_p / ms_u - 1.0), "gemm_ms_per_step": ms_p,
+           "cublas_unprotected_tflops": flops / (ms_c * 1e-3) / 1e12,
+           "protected_vs_cublas_pct": 100.0 * (ms_p / ms_c - 1.0),
            "l2": f"distinct per-layer buffers, {sum(ly['x'].numel() + ly['y'].numel() for ly in layers) * 2 / 1e9:.1f} "
                  f"GB of activations per step (>> 126 MB L2)"}
-    del layers, gp, gu
+    del layers, gp, gu, gc
     torch.cuda.empty_cache()
     return out
 
