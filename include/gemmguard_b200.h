@@ -107,7 +107,10 @@ typedef struct gg_gemm_desc {
   void* C; int64_t ldc;       /* elements */
 
   int32_t protect;            /* 0: unprotected baseline of the same kernel  */
-  int32_t chk_prec;           /* GG_P_F64 (float kinds) or GG_P_I64 (GG_I8)  */
+  int32_t chk_prec;           /* GG_P_F64 / F32 / F16 (float kinds: d is formed in
+                                 double-float and reported in binary64 for all
+                                 three, at least the reference's precision) or
+                                 GG_P_I64 (GG_I8)                               */
   const void* w_sum;          /* [K] f64 or i64: gg_offline_checksum output  */
   const void* w_aux;          /* gg_checksum_aux output for this ab_kind     */
   double bias_sum_f;          /* bias_sum for GG_P_F64                       */

@@ -314,8 +314,11 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   if (protect || replay) {
     if (int_kind && d->chk_prec != GG_P_I64)
       return fail(GG_EINVAL, "integer layers require the int64-exact checksum precision");
-    if (!int_kind && d->chk_prec != GG_P_F64)
-      return fail(GG_EUNSUPPORTED, "fused checksum supports binary64 precision for float kinds (use gg_verify_rows)");
+    // float kinds: d is formed in double-float and rounded once to binary64 whatever the
+    // requested checksum precision (binary16 / binary32 / binary64): at least as precise as the
+    // reference's folds in that precision (guard.py:135-139), never less
+    if (!int_kind && d->chk_prec != GG_P_F64 && d->chk_prec != GG_P_F32 && d->chk_prec != GG_P_F16)
+      return fail(GG_EINVAL, "float layers take a floating checksum precision");
     if (reinterpret_cast<uintptr_t>(d->w_sum) & 15) return fail(GG_EINVAL, "protected_gemm: w_sum must be 16-byte aligned");
     if (d->w_aux == nullptr || (reinterpret_cast<uintptr_t>(d->w_aux) & 15))
       return fail(GG_EINVAL, "protected_gemm: w_aux (gg_checksum_aux) is required and must be 16-byte aligned");
@@ -361,6 +364,9 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.C = d->C;
   p.ldc = d->ldc;
   p.c_tma = c_tma;
+#ifdef GG_DIAGNOSTICS
+  if (std::getenv("GG_NO_CTMA")) p.c_tma = 0;  // diagnostics: direct vector stores from registers
+#endif
   {
     static const int dbg = [] {
       const char* e = std::getenv("GG_DEBUG");

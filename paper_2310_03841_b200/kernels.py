@@ -168,7 +168,8 @@ def build_desc(
     d.C, d.ldc = y.data_ptr(), y.stride(0)
     d.protect = 1 if protect else 0
     integer = x.dtype == torch.int8
-    d.chk_prec = L.GG_P_I64 if integer else L.GG_P_F64
+    d.chk_prec = L.GG_P_I64 if integer else {torch.float32: L.GG_P_F32, torch.float16: L.GG_P_F16}.get(
+        None if w_sum is None else w_sum.dtype, L.GG_P_F64)
     if protect:
         d.w_sum = _ptr(w_sum)
         d.w_aux = _ptr(w_aux)
@@ -238,6 +239,8 @@ def checksum_aux(w_sum: torch.Tensor, ab_dtype: torch.dtype, f32_mode: str = "3x
     nbytes = int(L.load().gg_checksum_aux_bytes(kind, K))
     if nbytes == 0:
         return None
+    if kind != L.GG_I8 and w_sum.dtype != torch.float64:  # binary16 / binary32 checksum precisions
+        w_sum = w_sum.to(torch.float64)
     aux = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     L.check(L.load().gg_checksum_aux(kind, w_sum.data_ptr(), K, aux.data_ptr(), _stream(dev)), "gg_checksum_aux")
     return aux

@@ -255,14 +255,44 @@ def make_sampler():
                                                   "cases": out}))
 
 
+PRECISION_CASES = [  # build_toy_model args (blocks, dim, tokens, classes, seed, dtype), dataset (size, seed)
+    ([1, 8, 4, 5, 3, "binary16-emulated"], [12, 1]),
+    ([2, 16, 6, 4, 5, "binary16-emulated"], [10, 2]),
+    ([1, 64, 8, 10, 7, "binary16-emulated"], [8, 3]),
+    ([2, 32, 8, 6, 9, "binary32"], [8, 4]),
+    ([1, 128, 4, 10, 11, "binary32"], [6, 5]),
+    ([1, 8, 4, 5, 3, "int8"], [12, 1]),
+]
+
+
+def make_precision():
+    """guard.choose_checksum_precision on toy models with the reference's own range profiles;
+    plus a degenerate (near-zero span) profile that exhausts every precision (binary64 fallback + warning)."""
+    import warnings
+
+    cases = []
+    for args, data in PRECISION_CASES:
+        model = Mo.build_toy_model(*args)
+        ds = Mo.make_synthetic_dataset(model, *data)
+        ranges = Pr.profile_ranges(model, ds)
+        for label, bounds in (("profiled", ranges.bounds),
+                              ("narrow", {i: (lo, lo + 1e-30) for i, (lo, hi) in ranges.bounds.items()})):
+            with warnings.catch_warnings(record=True) as w:
+                warnings.simplefilter("always")
+                got = G.choose_checksum_precision(model, Pr.RangeProfile(dict(bounds)))
+            cases.append({"args": args, "ranges": {str(k): list(v) for k, v in bounds.items()}, "label": label,
+                          "chosen": {str(k): v.value for k, v in got.items()},
+                          "warnings": [str(x.message) for x in w]})
+    (OUT / "precision.json").write_text(json.dumps({"cases": cases}, indent=1))
+
+
 if __name__ == "__main__":
     import numpy
 
-    make_gemm()
-    make_checksum()
-    make_sampler()
-    make_toys()
-    make_cfg1()
+    parts = sys.argv[1:] or ["gemm", "checksum", "sampler", "toys", "cfg1", "precision"]
+    for part in parts:
+        {"gemm": make_gemm, "checksum": make_checksum, "sampler": make_sampler, "toys": make_toys,
+         "cfg1": make_cfg1, "precision": make_precision}[part]()
     (OUT / "VERSIONS.json").write_text(json.dumps({"numpy": numpy.__version__, "python": sys.version.split()[0],
                                                     "reference": str(REF)}))
     print("golden fixtures written to", OUT)

@@ -389,3 +389,35 @@ def test_int8_campaign(fp32_bench):
     for rec in run_campaign(model, golden, ranges, 10, seed=9).records:
         lo, hi = ranges.bounds[rec.spec.layer_index]
         assert isinstance(rec.original_value, int) and lo <= rec.corrupted_value <= hi
+
+
+def test_fused_check_takes_the_chosen_checksum_precisions(fp16_bench):
+    """choose_checksum_precision's binary32 / binary16 picks run the fused check (no extra verify
+    pass); its d stays within the reference-precision fold's error of the reference d, and a fault
+    is still detected."""
+    from paper_2310_03841_b200 import guard as GG
+    from paper_2310_03841_b200.model import CheckedOutput
+
+    model, golden, ranges, _, _ = fp16_bench
+    for p in (Precision.BINARY32, Precision.BINARY16):
+        chks = {L.index: offline_checksum(L, p) for L in model.layers}
+        eps = calibrate_epsilon(model, golden, precisions=p, confidence=0.9999)
+        sid = golden.sample_ids[0]
+        x, label = golden.input_for(sid), golden.labels[sid]
+        seen = []
+        real = GG._verify_arrays
+
+        def spy(xin, y, chk, e):
+            seen.append(isinstance(y, CheckedOutput) and y.fused_verdict() is not None)
+            return real(xin, y, chk, e)
+
+        GG._verify_arrays = spy
+        try:
+            _, events = protected_forward(model, x, label, list(range(len(model.layers))), chks, eps, None,
+                                          record_all=True)
+        finally:
+            GG._verify_arrays = real
+        assert seen and all(seen)  # every check came from the fused launch
+        spec = InjectionSpec(2, "output", 3, 14, "fp_exponent_bit", sid, 0)
+        _, events = protected_forward(model, x, label, list(range(len(model.layers))), chks, eps, None, inject=spec)
+        assert [e.layer_index for e in events if e.triggered] == [2]
