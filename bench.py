@@ -320,7 +320,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict:
 
     from paper_2310_03841_b200.vit import VIT_B16, ProtectedViT
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
     cfg = VIT_B16
@@ -524,9 +524,16 @@ def main():
     import torch
 
     if world > 1:
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr: one rank per GPU, NVLink paths
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # one rank per GPU over NCCL; GG_BENCH_BACKEND=gloo lets several ranks share one GPU to
+        # exercise the N > 1 path where only one GPU is visible (tests / single-GPU boxes)
+        backend = os.environ.get("GG_BENCH_BACKEND", "nccl")
+        dev = torch.device("cuda", local_rank % torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr: one rank per GPU
+            torch.distributed.init_process_group("nccl", device_id=dev)
+        else:
+            torch.distributed.init_process_group(backend)
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline:

@@ -125,6 +125,8 @@ def merge_stats(local: RunningStats) -> Moments:
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return local.moments()
     t = local.state.detach().to(torch.float64)
+    if dist.get_backend() == "gloo":  # gloo gathers host tensors
+        t = t.cpu()
     parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(parts, t)
     return merge_moments([Moments(*p.tolist()) for p in parts])
