@@ -31,7 +31,6 @@ from dataclasses import dataclass
 import torch
 import torch.nn.functional as F
 
-from . import _lib as L
 from . import kernels as K
 from .calib import RunningStats
 from .vit import ProtectedLinear

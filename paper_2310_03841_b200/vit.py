@@ -96,9 +96,6 @@ class ViTConfig:
 VIT_B16 = ViTConfig()
 VIT_L16 = ViTConfig(name="vit_l16", dim=1024, depth=24, heads=16, mlp=4096)
 
-_ROWS_PER_IMAGE = "tokens"  # rows of layer outputs per image: tokens (patch embed: tokens - 1, head: 1)
-
-
 class ProtectedLinear(torch.nn.Module):
     """y = x @ W.T + b as one protected GEMM launch (K1) with a device-resident check.
 
