@@ -286,13 +286,25 @@ def make_precision():
     (OUT / "precision.json").write_text(json.dumps({"cases": cases}, indent=1))
 
 
+def make_albt():
+    """weights_io.save_weights of two toy models: the ALBT fixtures of tests/test_albt_*.py."""
+    from gemmguard import weights_io as W
+
+    for name, args in (("toy_fp16.albt", [1, 8, 4, 5, 3, "binary16-emulated"]), ("toy_int8.albt", [2, 8, 4, 5, 7, "int8"]),
+                       ("toy_fp32.albt", [1, 12, 5, 4, 9, "binary32"])):
+        W.save_weights(OUT / name, Mo.build_toy_model(*args))
+    (OUT / "albt.json").write_text(json.dumps({"toy_fp16.albt": [1, 8, 4, 5, 3, "binary16-emulated"],
+                                               "toy_int8.albt": [2, 8, 4, 5, 7, "int8"],
+                                               "toy_fp32.albt": [1, 12, 5, 4, 9, "binary32"]}))
+
+
 if __name__ == "__main__":
     import numpy
 
-    parts = sys.argv[1:] or ["gemm", "checksum", "sampler", "toys", "cfg1", "precision"]
+    parts = sys.argv[1:] or ["gemm", "checksum", "sampler", "toys", "cfg1", "precision", "albt"]
     for part in parts:
         {"gemm": make_gemm, "checksum": make_checksum, "sampler": make_sampler, "toys": make_toys,
-         "cfg1": make_cfg1, "precision": make_precision}[part]()
+         "cfg1": make_cfg1, "precision": make_precision, "albt": make_albt}[part]()
     (OUT / "VERSIONS.json").write_text(json.dumps({"numpy": numpy.__version__, "python": sys.version.split()[0],
                                                     "reference": str(REF)}))
     print("golden fixtures written to", OUT)

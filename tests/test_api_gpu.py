@@ -421,3 +421,23 @@ def test_fused_check_takes_the_chosen_checksum_precisions(fp16_bench):
         spec = InjectionSpec(2, "output", 3, 14, "fp_exponent_bit", sid, 0)
         _, events = protected_forward(model, x, label, list(range(len(model.layers))), chks, eps, None, inject=spec)
         assert [e.layer_index for e in events if e.triggered] == [2]
+
+
+@pytest.mark.parametrize("name", ["toy_fp16.albt", "toy_int8.albt", "toy_fp32.albt"])
+def test_albt_loads_into_device_memory(name):
+    """One host->device transfer of the reference-written container; device weights in K1's
+    [out, in] layout equal the host model's; K2 on the device gives the reference checksums."""
+    import torch
+
+    from paper_2310_03841_b200 import albt
+    from tests.golden_io import GOLDEN
+
+    model = albt.load_model(GOLDEN / name)
+    dw = albt.load_device(GOLDEN / name)
+    for ly in model.layers:
+        w = dw.weights[ly.index].cpu().numpy()
+        assert np.array_equal(w.T.astype(np.float64), ly.weight.widened())
+        p = Precision.INT64 if model.is_integer else Precision.BINARY64
+        chk = offline_checksum(ly, p)
+        assert dw.w_sum[ly.index].cpu().numpy().tobytes() == chk.w_sum.tobytes()
+        assert dw.bias_sum[ly.index] == chk.bias_sum
