@@ -106,6 +106,36 @@ __device__ __forceinline__ void pair_range(int pid, int npairs, int total, int& 
   t1 = static_cast<int>(static_cast<long long>(pid + 1) * total / npairs);
 }
 
+// d / flag / gap key of one row from its folded sums (guard.py:163-171, 188-215).  Flags follow
+// the per-sample rule; a batch_mean launch has its flags re-derived from every d by the
+// launcher's follow-up pass (NumPy's pairwise mean, guard.py:198-201).
+template <bool INT>
+__device__ __forceinline__ void row_check(const Params& p, unsigned long long obs, unsigned long long pred,
+                                          unsigned long long& dbits, bool& flag, unsigned long long& key) {
+  if constexpr (INT) {
+    const long long di = (static_cast<long long>(pred) + p.bias_sum_i) - static_cast<long long>(obs);
+    dbits = static_cast<unsigned long long>(di);
+    flag = di != 0;
+    const unsigned long long mag =
+        di < 0 ? 0ull - static_cast<unsigned long long>(di) : static_cast<unsigned long long>(di);
+    key = f64_bits_of_u64(mag) + 1ull;  // gap_key(double(|d|))
+  } else {
+    // d = (pred + bias) - obs in double-float, one rounding to binary64 (no FP64 instruction)
+    const unsigned long long dd = df_add(df_add(pred, p.bias_df), obs ^ 0x8000000080000000ull);
+    const unsigned long long db = f64_bits_of_df_norm(dd);
+    dbits = db;
+    const unsigned long long ok = f64_order_key(db);
+    flag = f64_bits_nan(db) || ok < p.lo_key || ok > p.hi_key;  // !(lo <= d <= hi)
+    unsigned long long gb = db & 0x7fffffffffffffffull;         // |d - mu|
+    if (!p.mu_zero) {
+      unsigned long long g = df_add(dd, p.neg_mu_df);
+      if (static_cast<uint32_t>(g) >> 31) g ^= 0x8000000080000000ull;
+      gb = f64_bits_of_df_norm(g);
+    }
+    key = f64_bits_nan(gb) ? 0ull : gb + 1ull;  // gap_key
+  }
+}
+
 // d / flags of the rows lane + 32q (q < 4) of band mb from their folded sums, with the
 // band's flag count and largest gap key reduced over the warp (no stores).
 template <bool INT>
@@ -116,8 +146,6 @@ struct BandRows {
   unsigned long long key;
 };
 
-// Flags follow the per-sample rule; a batch_mean launch has its flags re-derived from
-// every d by the launcher's follow-up pass (NumPy's pairwise mean, guard.py:198-201).
 template <bool INT>
 __device__ __forceinline__ BandRows<INT> band_rows(const Params& p, int mb, int lane, const unsigned long long (&obs)[4],
                                                   const unsigned long long (&pred)[4]) {
@@ -130,30 +158,9 @@ __device__ __forceinline__ BandRows<INT> band_rows(const Params& p, int mb, int 
     r.flag[q] = false;
     r.dbits[q] = 0;
     if (row >= p.M) continue;
-    if constexpr (INT) {
-      const long long di = (static_cast<long long>(pred[q]) + p.bias_sum_i) - static_cast<long long>(obs[q]);
-      r.dbits[q] = static_cast<unsigned long long>(di);
-      r.flag[q] = di != 0;
-      const unsigned long long mag =
-          di < 0 ? 0ull - static_cast<unsigned long long>(di) : static_cast<unsigned long long>(di);
-      const unsigned long long k = f64_bits_of_u64(mag) + 1ull;  // gap_key(double(|d|))
-      r.key = k > r.key ? k : r.key;
-    } else {
-      // d = (pred + bias) - obs in double-float, one rounding to binary64 (no FP64 instruction)
-      const unsigned long long dd = df_add(df_add(pred[q], p.bias_df), obs[q] ^ 0x8000000080000000ull);
-      const unsigned long long db = f64_bits_of_df_norm(dd);
-      r.dbits[q] = db;
-      const unsigned long long ok = f64_order_key(db);
-      r.flag[q] = f64_bits_nan(db) || ok < p.lo_key || ok > p.hi_key;  // !(lo <= d <= hi)
-      unsigned long long gb = db & 0x7fffffffffffffffull;                // |d - mu|
-      if (!p.mu_zero) {
-        unsigned long long g = df_add(dd, p.neg_mu_df);
-        if (static_cast<uint32_t>(g) >> 31) g ^= 0x8000000080000000ull;
-        gb = f64_bits_of_df_norm(g);
-      }
-      const unsigned long long k = f64_bits_nan(gb) ? 0ull : gb + 1ull;  // gap_key
-      r.key = k > r.key ? k : r.key;
-    }
+    unsigned long long k;
+    row_check<INT>(p, obs[q], pred[q], r.dbits[q], r.flag[q], k);
+    r.key = k > r.key ? k : r.key;
     r.nflag += r.flag[q] ? 1 : 0;
   }
 #pragma unroll
@@ -447,6 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* fq_full = pempty_bar + NSLOT;       // [FQ] a split band id queued by the reducer
   uint64_t* fq_empty = fq_full + FQ;            // [FQ] taken by the finisher warp
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fq_empty + FQ);
+  int* tiny_last = reinterpret_cast<int*>(tmem_slot + 1);         // this CTA folds a tiny launch
   int* fq_band = reinterpret_cast<int*>(tmem_slot + 4);           // [FQ]
   double* slot_obs = reinterpret_cast<double*>(tmem_slot + QAREA / 4);  // [NSLOT][2 halves][BM] (int64 bits for INT)
   double* slot_pred = slot_obs + 2 * NSLOT * BM;                // [NSLOT][BM]
@@ -605,6 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       mbar_init(&fq_full[b], 1);
       mbar_init(&fq_empty[b], 1);
     }
+    tiny_last[0] = 0;
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -795,20 +804,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             // the pair's last tile of this band: release its partials with one count of the
             // tiles it contributed (contiguous schedule: at most two such parts per pair).
             // Tiny launches (at most one tile per pair) count on one launch-wide counter and
-            // the last tile of the launch folds every band and publishes the summary itself.
+            // the CTA of the launch's last tile folds every row with all its threads once its
+            // roles are done (after the kernel's closing barrier, below).
             const int part = (p.sched || p.tiny) ? 1 : min((m + 1) * n_tiles, t1) - max(m * n_tiles, t0);
             int* counter = p.tiny ? &p.ws.counters[3] : &p.ws.band_counter[mb];
             __syncwarp();
             int last = 0;
             if (lane == 0) {
+#ifdef GG_TRACE
+              const long long tt_a = clock64();
+#endif
               const int total = p.tiny ? n_tiles * (p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles) : n_tiles;
-              const int prev = GG_DBG(16) ? atomicAdd(counter, part) : atom_add_release_gpu(counter, part);
+              // acquire-release add: our partials are visible before the count, and the last
+              // arriver sees every other pair's partials (no separate fence)
+              const int prev = GG_DBG(16) ? atomicAdd(counter, part) : atom_add_acq_rel_gpu(counter, part);
               // claim mode: only a tiny launch's last tile acts; the claimed band's finisher
               // waits for its count to reach n_tiles (one release sequence) and resets it
               last = ((!claim || p.tiny) && prev == total - part) ? 1 : 0;
               if (last) {
-                fence_acquire_gpu();  // the other pairs' partials
                 *counter = 0;
+                if (p.tiny) tiny_last[0] = 1;
+#ifdef GG_TRACE
+                if (p.tiny && g_trace != nullptr) {
+                  const size_t tb0 = static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV;
+                  g_trace[tb0 + 24] = tt_a;
+                  g_trace[tb0 + 25] = clock64();
+                }
+#endif
               }
             }
             last = __shfl_sync(0xffffffffu, last, 0);
@@ -820,57 +842,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 mbar_arrive(&fq_full[q]);
               }
               ++fq_i;
-            } else if (last && p.tiny) {
-              // every band's partials in one burst of async copies into this CTA's (now idle)
-              // pipeline stages: [band][tile][obs half 0, obs half 1, pred][128 rows]
-              // (m_tiles * n_tiles <= 48)
-              const uint32_t sbuf = smem_u32(smA);
-              for (int b = 0; b < p.m_tiles; ++b) {
-                if (p.replay && !p.ws.band_active[b]) continue;
-                for (int tt = 0; tt < n_tiles; ++tt) {
-                  const size_t g = static_cast<size_t>(tt) * p.m_pad + b * BM + 2 * lane;
-                  const uint32_t d0 = sbuf + static_cast<uint32_t>(((b * n_tiles + tt) * 3) * BM * 8 + lane * 16);
-#pragma unroll
-                  for (int h = 0; h < 2; ++h) {  // rows 2*lane + 64h .. +1
-                    cp_async16(d0 + h * 512, gpart + g + 64 * h);
-                    cp_async16(d0 + BM * 8 + h * 512, gpart + half_stride + g + 64 * h);
-                    cp_async16(d0 + 2 * BM * 8 + h * 512, gpred + g + 64 * h);
-                  }
-                }
-              }
-              cp_async_wait_all();
-              __syncwarp();
-              const unsigned long long* sv = reinterpret_cast<const unsigned long long*>(smA);
-              int nf = 0;
-              unsigned long long mk = 0;
-              for (int b = 0; b < p.m_tiles; ++b) {
-                if (p.replay && !p.ws.band_active[b]) {
-                  nf += __ldcg(&p.ws.band_nflag[b]);  // standing summary of an untouched band
-                  const unsigned long long k = __ldcg(&p.ws.band_maxkey[b]);
-                  mk = k > mk ? k : mk;
-                  continue;
-                }
-                unsigned long long bo[4], bpr[4], b0[4] = {0ull, 0ull, 0ull, 0ull}, b1[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) bpr[q] = 0ull;
-                for (int tt = 0; tt < n_tiles; ++tt) {  // ascending tiles per half, as fold_band
-                  const unsigned long long* base = sv + static_cast<size_t>((b * n_tiles + tt) * 3) * BM;
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    b0[q] = acc_add<OBS_MODE>(b0[q], base[lane + 32 * q]);
-                    b1[q] = acc_add<OBS_MODE>(b1[q], base[BM + lane + 32 * q]);
-                    bpr[q] = acc_add<PRED_MODE>(bpr[q], base[2 * BM + lane + 32 * q]);
-                  }
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) bo[q] = acc_add<OBS_MODE>(b0[q], b1[q]);
-                const BandRows<INT> r = band_rows<INT>(p, b, lane, bo, bpr);
-                store_band<INT>(p, b, lane, r);
-                nf += r.nflag;
-                mk = r.key > mk ? r.key : mk;
-              }
-              __syncwarp();
-              publish_summary<INT>(p, lane, nf, mk);
             }
           }
         }
@@ -1400,7 +1371,124 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  cluster_sync_all();  // the peer's smem / barriers / TMEM stay alive until both CTAs are done
+  if constexpr (PROTECT) {
+    if (p.tiny && tiny_last[0] && !GG_DBG(4096)) {
+      // Tiny launch, the CTA of its last tile: every row (m_tiles * BM <= 512, one per thread)
+      // folded from the workspace partials in the same association as fold_band (per column
+      // half over ascending tiles, then the halves), its d / flag stored, then the band and
+      // launch summaries.  The reducer's acquire-add and this barrier order the loads.
+#ifdef GG_TRACE
+      if (threadIdx.x == 0 && g_trace != nullptr) g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + 26] = clock64();
+#endif
+      const int r = threadIdx.x;
+      const int b = r / BM;
+      int nf = 0;
+      unsigned long long key = 0ull;
+      if (b < p.m_tiles && (!p.replay || p.ws.band_active[b])) {
+        unsigned long long b0 = 0ull, b1 = 0ull, bp = 0ull;
+        if (GG_DBG(512)) {
+          b0 = r; b1 = 2 * r; bp = 3 * r;
+        } else {
+          // TB tiles' loads in flight together (measured: 4 beats 8 / 12 and staging every
+          // partial in shared memory first, cp.async or bulk copies, even at 12 tiles)
+#ifndef GG_TINY_TB
+          constexpr int TB = 4;
+#else
+          constexpr int TB = GG_TINY_TB;
+#endif
+          for (int tt = 0; tt < n_tiles; tt += TB) {
+            unsigned long long v0[TB], v1[TB], vp[TB];
+#pragma unroll
+            for (int j = 0; j < TB; ++j) {
+              v0[j] = v1[j] = vp[j] = 0ull;
+              if (tt + j < n_tiles) {
+                const size_t g = static_cast<size_t>(tt + j) * p.m_pad + r;
+                v0[j] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpart + g)));
+                v1[j] = static_cast<unsigned long long>(
+                    ldcg_i64(reinterpret_cast<const long long*>(gpart + half_stride + g)));
+                vp[j] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpred + g)));
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < TB; ++j) {
+              if (tt + j >= n_tiles) break;
+              b0 = acc_add<OBS_MODE>(b0, v0[j]);
+              b1 = acc_add<OBS_MODE>(b1, v1[j]);
+              bp = acc_add<PRED_MODE>(bp, vp[j]);
+            }
+          }
+        }
+#ifdef GG_TRACE
+        if (threadIdx.x == 0 && g_trace != nullptr) {
+          if (b0 == 12345ull && b1 == 777ull && bp == 3ull) g_trace[0] = 0;  // the fold is done before the stamp
+          g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + TRACE_EV + 24] = clock64();
+        }
+#endif
+        if (r < p.M && !GG_DBG(16384)) {
+          unsigned long long db;
+          bool fl;
+          row_check<INT>(p, acc_add<OBS_MODE>(b0, b1), bp, db, fl, key);
+          static_cast<unsigned long long*>(p.d)[r] = db;
+          p.flags[r] = fl ? 1 : 0;
+          nf = fl ? 1 : 0;
+        }
+#ifdef GG_TRACE
+        if (threadIdx.x == 0 && g_trace != nullptr) {
+          if (key == 12345ull) g_trace[0] = 0;
+          g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + TRACE_EV + 25] = clock64();
+        }
+#endif
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        nf += __shfl_xor_sync(0xffffffffu, nf, o);
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, key, o);
+        key = w > key ? w : key;
+      }
+      // per-warp totals in the (idle) observed ring, [16] keys then [16] counts, by explicit
+      // shared-space accesses (a generic load here waits behind the warp's global stores)
+      const uint32_t red = smem_u32(slot_obs);
+      if (lane == 0) {
+        sts64(red + 8u * warp, key);
+        sts32(red + 128u + 4u * warp, static_cast<uint32_t>(nf));
+      }
+      __syncthreads();
+#ifdef GG_TRACE
+      if (threadIdx.x == 0 && g_trace != nullptr) g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + TRACE_EV + 26] = clock64();
+#endif
+      if (warp == 0) {  // lane b: band b (four warps per band), then the launch
+        int bn = 0;
+        unsigned long long bk = 0ull;
+        if (lane < p.m_tiles) {
+          if (p.replay && !p.ws.band_active[lane]) {  // standing summary of an untouched band
+            bn = __ldcg(&p.ws.band_nflag[lane]);
+            bk = __ldcg(&p.ws.band_maxkey[lane]);
+          } else {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              const int wi = 4 * lane + w;
+              bn += static_cast<int>(lds32(red + 128u + 4u * wi));
+              const unsigned long long k = lds64(red + 8u * wi);
+              bk = k > bk ? k : bk;
+            }
+            p.ws.band_nflag[lane] = bn;
+            p.ws.band_maxkey[lane] = bk;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          bn += __shfl_xor_sync(0xffffffffu, bn, o);
+          const unsigned long long w = __shfl_xor_sync(0xffffffffu, bk, o);
+          bk = w > bk ? w : bk;
+        }
+        publish_summary<INT>(p, lane, bn, bk);
+#ifdef GG_TRACE
+        if (lane == 0 && g_trace != nullptr) g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + 27] = clock64();
+#endif
+      }
+    }
+  }
+  cluster_sync_exit();  // the peer's smem / barriers / TMEM stay alive until both CTAs are done
   if (warp == W_ALLOC) tmem_dealloc_pair(tmem_base, TMEM_COLS);
 }
 

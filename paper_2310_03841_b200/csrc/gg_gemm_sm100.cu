@@ -441,8 +441,9 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   if (p.dbg & 2048) p.sched = 1;
 #endif
   if (replay) p.sched = 1;  // replay walks the listed band pairs strided; every band folds via the workspace
-  // tiny launches (at most one tile per pair, few bands): one launch-wide fold from smem
-  p.tiny = (pair_tiles <= pairs && p.m_tiles <= 4 && p.m_tiles * p.n_tiles <= 48) ? 1 : 0;
+  // tiny launches (at most one tile per pair, <= 4 bands): one launch-wide count, every row
+  // folded by the threads of the last arriving CTA
+  p.tiny = (pair_tiles <= pairs && p.m_tiles <= 4) ? 1 : 0;  // one fold thread per row (<= 512)
   p.one_tile = (pair_tiles <= pairs && !replay) ? 1 : 0;
 
   switch (kind) {

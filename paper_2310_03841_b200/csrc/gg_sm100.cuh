@@ -28,6 +28,14 @@ __device__ __forceinline__ int atom_add_release_gpu(int* addr, int v) {
   asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
   return old;
 }
+// Acquire-release add at GPU scope: the release above, and this thread's later reads see
+// what the other releasers wrote before their adds (the last-arriver pattern, one instruction
+// instead of a release-add plus a separate acquire fence).
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* addr, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ unsigned long long atom_add_release_gpu_u64(unsigned long long* addr,
                                                                       unsigned long long v) {
   unsigned long long old;
@@ -192,6 +200,12 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t a, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// The closing rendezvous of a pair: only lifetime (the peer's shared memory, barriers and TMEM
+// stay allocated until both CTAs are done), no data handed over, so a relaxed arrive -- the
+// release form is a MEMBAR.ALL.GPU per warp at the very end of the kernel.
+__device__ __forceinline__ void cluster_sync_exit() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 // arrive on an mbarrier given by its shared::cluster address (may be in the peer CTA).
 // Default (.release.cta) semantics: the only data handed over is TMEM, ordered by
 // tcgen05.fence::before_thread_sync; a .cluster-scope release would compile to a
@@ -311,6 +325,22 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
 }
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void sts64(uint32_t addr, unsigned long long v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long lds64(uint32_t addr) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
 }
 
 // ---------------------------------------------------------------- misc
