@@ -199,6 +199,22 @@ __device__ void publish_summary(const Params& p, int lane, int nf, unsigned long
   }
 }
 
+// Finished bands' count into the launch summary: atomicMax of their gap key, then an
+// acquire-release add of {bands << 32 | flagged rows}; true in the call that completes the count,
+// with the launch totals.  (The callers store the band's rows after it: the release then has
+// no outstanding stores to wait for.)
+__device__ __forceinline__ bool launch_count(const Params& p, int bands, int nflag, unsigned long long key,
+                                             unsigned long long& fin_rows, unsigned long long& fin_key) {
+  const int total = p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles;
+  atomicMax(&p.ws.summary[1], key);
+  const unsigned long long inc = (static_cast<unsigned long long>(bands) << 32) | static_cast<unsigned>(nflag);
+  const unsigned long long old = atom_add_acq_rel_gpu_u64(&p.ws.summary[0], inc);
+  if (static_cast<long long>(old >> 32) + bands != total) return false;
+  fin_rows = (old + inc) & 0xFFFFFFFFull;
+  fin_key = atomicMax(&p.ws.summary[1], 0ull);
+  return true;
+}
+
 // d / flags of band mb, its band summary and, for the band that completes the launch's
 // count, the launch summaries (nflag, triggered, max_disc).  One warp.
 template <bool INT>
@@ -211,24 +227,9 @@ __device__ void finish_band(const Params& p, int mb, int lane, const unsigned lo
 #ifdef GG_TRACE
   const long long fb_t1 = clock64();
 #endif
-  // Launch summary: atomicMax of the band's gap key, then a release-add of
-  // {1 << 32 | flagged rows}; the band that completes the count acquires and reads the
-  // totals.  The release has no outstanding stores to wait for when the rows are stored
-  // after it.
   int last = 0;
   unsigned long long fin_rows = 0, fin_key = 0;
-  if (lane == 0 && !GG_DBG(8192)) {
-    const int total = p.replay ? __ldcg(&p.ws.counters[1]) : p.m_tiles;
-    atomicMax(&p.ws.summary[1], r.key);
-    const unsigned long long inc = (1ull << 32) | static_cast<unsigned>(r.nflag);
-    const unsigned long long old = atom_add_release_gpu_u64(&p.ws.summary[0], inc);
-    last = (static_cast<long long>(old >> 32) + 1 == total) ? 1 : 0;
-    if (last) {
-      fence_acquire_gpu();
-      fin_rows = (old + inc) & 0xFFFFFFFFull;
-      fin_key = atomicMax(&p.ws.summary[1], 0ull);
-    }
-  }
+  if (lane == 0 && !GG_DBG(8192)) last = launch_count(p, 1, r.nflag, r.key, fin_rows, fin_key) ? 1 : 0;
 #ifdef GG_TRACE
   const long long fb_t2 = clock64();
 #endif
@@ -454,7 +455,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* fq_full = pempty_bar + NSLOT;       // [FQ] a split band id queued by the reducer
   uint64_t* fq_empty = fq_full + FQ;            // [FQ] taken by the finisher warp
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fq_empty + FQ);
-  int* tiny_last = reinterpret_cast<int*>(tmem_slot + 1);         // this CTA folds a tiny launch
+  int* end_fold = reinterpret_cast<int*>(tmem_slot + 1);  // the kernel-end fold: [0] 0 none, 1 every row,
+                                                          // 1 + k: the k bands [1], [2]
   int* fq_band = reinterpret_cast<int*>(tmem_slot + 4);           // [FQ]
   double* slot_obs = reinterpret_cast<double*>(tmem_slot + QAREA / 4);  // [NSLOT][2 halves][BM] (int64 bits for INT)
   double* slot_pred = slot_obs + 2 * NSLOT * BM;                // [NSLOT][BM]
@@ -551,42 +553,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int q = 0; q < 4; ++q) bo[q] = acc_add<OBS_MODE>(b0[q], b1[q]);
   };
-  // The same fold from one burst of async copies into this CTA's pipeline stages, for
-  // launches with at most one tile per pair (a band's finisher CTA has no tile in flight):
-  // one round trip instead of n_tiles / FB.  Layout [tile][half 0, half 1, pred][128 rows].
-  const bool burst_fold = p.one_tile && 3 * n_tiles * BM * 8 <= STAGES * (A_BYTES + B_BYTES);
-  auto fold_band_burst = [&](int b, unsigned long long (&bo)[4], unsigned long long (&bpr)[4]) {
-    const uint32_t sbuf = smem_u32(smA);
-    for (int tt = 0; tt < n_tiles; ++tt) {
-      const size_t g = static_cast<size_t>(tt) * p.m_pad + b * BM + 2 * lane;
-      const uint32_t d0 = sbuf + static_cast<uint32_t>(tt * 3 * BM * 8 + lane * 16);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {  // rows 2*lane + 64h .. +1
-        cp_async16(d0 + h * 512, gpart + g + 64 * h);
-        cp_async16(d0 + BM * 8 + h * 512, gpart + half_stride + g + 64 * h);
-        cp_async16(d0 + 2 * BM * 8 + h * 512, gpred + g + 64 * h);
-      }
-    }
-    cp_async_wait_all();
-    __syncwarp();
-    const unsigned long long* sv = reinterpret_cast<const unsigned long long*>(smA);
-    unsigned long long b0[4] = {0ull, 0ull, 0ull, 0ull}, b1[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) bpr[q] = 0ull;
-    for (int tt = 0; tt < n_tiles; ++tt) {  // ascending tiles per half, as fold_band
-      const unsigned long long* base = sv + static_cast<size_t>(tt * 3) * BM;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        b0[q] = acc_add<OBS_MODE>(b0[q], base[lane + 32 * q]);
-        b1[q] = acc_add<OBS_MODE>(b1[q], base[BM + lane + 32 * q]);
-        bpr[q] = acc_add<PRED_MODE>(bpr[q], base[2 * BM + lane + 32 * q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) bo[q] = acc_add<OBS_MODE>(b0[q], b1[q]);
-    __syncwarp();
-  };
-
   // warp roles; the SMSP arbiter issues highest-warp-id first, so the ids follow criticality
   constexpr int W_MMA = 15, W_PRODUCER = 14, W_ALLOC = 13, W_REDUCER = 12, W_CHK0 = 8, W_EPI0 = 0;
   if (warp == W_PRODUCER && lane == 0) {
@@ -613,7 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       mbar_init(&fq_full[b], 1);
       mbar_init(&fq_empty[b], 1);
     }
-    tiny_last[0] = 0;
+    end_fold[0] = 0;
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -823,7 +789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               last = ((!claim || p.tiny) && prev == total - part) ? 1 : 0;
               if (last) {
                 *counter = 0;
-                if (p.tiny) tiny_last[0] = 1;
+                if (p.tiny) end_fold[0] = 1;
 #ifdef GG_TRACE
                 if (p.tiny && g_trace != nullptr) {
                   const size_t tb0 = static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV;
@@ -834,7 +800,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               }
             }
             last = __shfl_sync(0xffffffffu, last, 0);
-            if (last && !p.tiny && !GG_DBG(32)) {  // hand the fold to the finisher warp: the reducer keeps draining slots
+            if (last && !p.tiny && p.few_tiles && !GG_DBG(32)) {
+              // at most two tiles per pair: the band is folded at the end of the kernel by all the
+              // CTA's threads (at most two such bands per CTA, one per tile)
+              if (lane == 0) {
+                const int k = end_fold[0] == 0 ? 0 : end_fold[0] - 1;  // bands listed so far
+                end_fold[1 + k] = mb;
+                end_fold[0] = 2 + k;
+              }
+            } else if (last && !p.tiny && !GG_DBG(32)) {  // hand the fold to the finisher warp: the reducer keeps draining slots
               if (lane == 0) {
                 const int q = fq_i % FQ;
                 mbar_wait(&fq_empty[q], (static_cast<uint32_t>(fq_i / FQ) & 1u) ^ 1u);
@@ -909,8 +883,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lane == 0) mbar_arrive(&fq_empty[q]);
         if (mb < 0) break;
         unsigned long long bo[4], bpr[4];
-        if (burst_fold) fold_band_burst(mb, bo, bpr);
-        else fold_band(mb, bo, bpr);
+        fold_band(mb, bo, bpr);
         if (!GG_DBG(256)) finish(mb, bo, bpr);
       }
     }
@@ -1371,73 +1344,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if constexpr (PROTECT) {
-    if (p.tiny && tiny_last[0] && !GG_DBG(4096)) {
-      // Tiny launch, the CTA of its last tile: every row (m_tiles * BM <= 512, one per thread)
-      // folded from the workspace partials in the same association as fold_band (per column
-      // half over ascending tiles, then the halves), its d / flag stored, then the band and
-      // launch summaries.  The reducer's acquire-add and this barrier order the loads.
-#ifdef GG_TRACE
-      if (threadIdx.x == 0 && g_trace != nullptr) g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + 26] = clock64();
-#endif
-      const int r = threadIdx.x;
+  if constexpr (PROTECT && !CLAIM) {  // (claim launches have more than two tiles per pair)
+    const int ef = end_fold[0];
+    if (ef != 0 && !GG_DBG(4096)) {
+      // The kernel-end fold, by every thread of the CTA (its roles are done): a tiny launch's
+      // last CTA folds every row of the launch (m_tiles * BM <= 512, one per thread); in a
+      // launch of at most two tiles per pair, the CTA that completed a band's count folds that
+      // band (at most two).
+      // Same association as fold_band (per column half over ascending tiles, then the halves).
+      // The reducer's acquire-add and the barrier above order the loads.
+      const bool every_row = ef == 1;
+      const int nb = every_row ? p.m_tiles : ef - 1;  // bands folded here
+      const int nrows = nb * BM;
+      const int tj = min(static_cast<int>(threadIdx.x) / BM, 1);
+      const int r = every_row ? static_cast<int>(threadIdx.x) : end_fold[1 + tj] * BM + static_cast<int>(threadIdx.x) % BM;
       const int b = r / BM;
       int nf = 0;
-      unsigned long long key = 0ull;
-      if (b < p.m_tiles && (!p.replay || p.ws.band_active[b])) {
+      unsigned long long key = 0ull, db = 0ull;
+      bool fl = false, mine = false;
+      if (static_cast<int>(threadIdx.x) < nrows && b < p.m_tiles && (!p.replay || p.ws.band_active[b])) {
         unsigned long long b0 = 0ull, b1 = 0ull, bp = 0ull;
-        if (GG_DBG(512)) {
-          b0 = r; b1 = 2 * r; bp = 3 * r;
-        } else {
-          // TB tiles' loads in flight together (measured: 4 beats 8 / 12 and staging every
-          // partial in shared memory first, cp.async or bulk copies, even at 12 tiles)
-#ifndef GG_TINY_TB
-          constexpr int TB = 4;
-#else
-          constexpr int TB = GG_TINY_TB;
-#endif
-          for (int tt = 0; tt < n_tiles; tt += TB) {
-            unsigned long long v0[TB], v1[TB], vp[TB];
+        // four tiles' loads in flight together (measured: 4 beats 2 / 8 / 12 and staging every
+        // partial in shared memory first, by cp.async or bulk copies, even at 12 tiles)
+        constexpr int TB = 4;
+        for (int tt = 0; tt < n_tiles; tt += TB) {
+          unsigned long long v0[TB], v1[TB], vp[TB];
 #pragma unroll
-            for (int j = 0; j < TB; ++j) {
-              v0[j] = v1[j] = vp[j] = 0ull;
-              if (tt + j < n_tiles) {
-                const size_t g = static_cast<size_t>(tt + j) * p.m_pad + r;
-                v0[j] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpart + g)));
-                v1[j] = static_cast<unsigned long long>(
-                    ldcg_i64(reinterpret_cast<const long long*>(gpart + half_stride + g)));
-                vp[j] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpred + g)));
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < TB; ++j) {
-              if (tt + j >= n_tiles) break;
-              b0 = acc_add<OBS_MODE>(b0, v0[j]);
-              b1 = acc_add<OBS_MODE>(b1, v1[j]);
-              bp = acc_add<PRED_MODE>(bp, vp[j]);
+          for (int j = 0; j < TB; ++j) {
+            v0[j] = v1[j] = vp[j] = 0ull;
+            if (tt + j < n_tiles) {
+              const size_t g = static_cast<size_t>(tt + j) * p.m_pad + r;
+              v0[j] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpart + g)));
+              v1[j] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpart + half_stride + g)));
+              vp[j] = static_cast<unsigned long long>(ldcg_i64(reinterpret_cast<const long long*>(gpred + g)));
             }
           }
+#pragma unroll
+          for (int j = 0; j < TB; ++j) {
+            if (tt + j >= n_tiles) break;
+            b0 = acc_add<OBS_MODE>(b0, v0[j]);
+            b1 = acc_add<OBS_MODE>(b1, v1[j]);
+            bp = acc_add<PRED_MODE>(bp, vp[j]);
+          }
         }
-#ifdef GG_TRACE
-        if (threadIdx.x == 0 && g_trace != nullptr) {
-          if (b0 == 12345ull && b1 == 777ull && bp == 3ull) g_trace[0] = 0;  // the fold is done before the stamp
-          g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + TRACE_EV + 24] = clock64();
-        }
-#endif
-        if (r < p.M && !GG_DBG(16384)) {
-          unsigned long long db;
-          bool fl;
+        if (r < p.M) {
           row_check<INT>(p, acc_add<OBS_MODE>(b0, b1), bp, db, fl, key);
-          static_cast<unsigned long long*>(p.d)[r] = db;
-          p.flags[r] = fl ? 1 : 0;
           nf = fl ? 1 : 0;
+          mine = true;
         }
-#ifdef GG_TRACE
-        if (threadIdx.x == 0 && g_trace != nullptr) {
-          if (key == 12345ull) g_trace[0] = 0;
-          g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + TRACE_EV + 25] = clock64();
-        }
-#endif
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1453,16 +1407,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         sts32(red + 128u + 4u * warp, static_cast<uint32_t>(nf));
       }
       __syncthreads();
-#ifdef GG_TRACE
-      if (threadIdx.x == 0 && g_trace != nullptr) g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + TRACE_EV + 26] = clock64();
-#endif
-      if (warp == 0) {  // lane b: band b (four warps per band), then the launch
+      if (warp == 0) {
+        // lane j: the j-th band folded here (four warps each)
         int bn = 0;
         unsigned long long bk = 0ull;
-        if (lane < p.m_tiles) {
-          if (p.replay && !p.ws.band_active[lane]) {  // standing summary of an untouched band
-            bn = __ldcg(&p.ws.band_nflag[lane]);
-            bk = __ldcg(&p.ws.band_maxkey[lane]);
+        if (lane < nb) {
+          const int bj = every_row ? lane : end_fold[1 + lane];
+          if (p.replay && !p.ws.band_active[bj]) {  // standing summary of an untouched band
+            bn = __ldcg(&p.ws.band_nflag[bj]);
+            bk = __ldcg(&p.ws.band_maxkey[bj]);
           } else {
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
@@ -1471,8 +1424,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               const unsigned long long k = lds64(red + 8u * wi);
               bk = k > bk ? k : bk;
             }
-            p.ws.band_nflag[lane] = bn;
-            p.ws.band_maxkey[lane] = bk;
+            p.ws.band_nflag[bj] = bn;
+            p.ws.band_maxkey[bj] = bk;
           }
         }
 #pragma unroll
@@ -1481,10 +1434,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const unsigned long long w = __shfl_xor_sync(0xffffffffu, bk, o);
           bk = w > bk ? w : bk;
         }
-        publish_summary<INT>(p, lane, bn, bk);
-#ifdef GG_TRACE
-        if (lane == 0 && g_trace != nullptr) g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + 27] = clock64();
-#endif
+        if (every_row) {
+          publish_summary<INT>(p, lane, bn, bk);
+        } else {  // the band into the launch count; the band completing it publishes
+          int last = 0;
+          unsigned long long fin_rows = 0, fin_key = 0;
+          if (lane == 0) last = launch_count(p, nb, bn, bk, fin_rows, fin_key) ? 1 : 0;
+          last = __shfl_sync(0xffffffffu, last, 0);
+          if (last) {
+            publish_summary<INT>(p, lane, static_cast<int>(__shfl_sync(0xffffffffu, fin_rows, 0)),
+                                 __shfl_sync(0xffffffffu, fin_key, 0));
+            if (lane == 0) {
+              p.ws.summary[0] = 0ull;  // every band has counted: the workspace is left ready
+              p.ws.summary[1] = 0ull;
+            }
+          }
+        }
+      }
+      if (mine) {  // the rows, after the counts (no outstanding stores for the release to wait on)
+        static_cast<unsigned long long*>(p.d)[r] = db;
+        p.flags[r] = fl ? 1 : 0;
       }
     }
   }

@@ -269,7 +269,7 @@ int dispatch_protect(bool protect, int act, const CUtensorMap& ta, const CUtenso
   if (act != GG_ACT_NONE) return fail(GG_EUNSUPPORTED, "protected_gemm: epilogue activation needs bf16 or fp16 outputs");
   if (!protect) return launch_pair_instance<KIND, OUT, false>(ta, tb, tc, p, grid, s);
   if constexpr (KIND == K_TF32) {  // claimed split-band folds (see the kernel)
-    if (!p.one_tile && p.n_tiles >= 8) return launch_pair_instance<KIND, OUT, true, true>(ta, tb, tc, p, grid, s);
+    if (!p.few_tiles && !p.tiny && p.n_tiles >= 8) return launch_pair_instance<KIND, OUT, true, true>(ta, tb, tc, p, grid, s);
   }
   return launch_pair_instance<KIND, OUT, true>(ta, tb, tc, p, grid, s);
 }
@@ -444,7 +444,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   // tiny launches (at most one tile per pair, <= 4 bands): one launch-wide count, every row
   // folded by the threads of the last arriving CTA
   p.tiny = (pair_tiles <= pairs && p.m_tiles <= 4) ? 1 : 0;  // one fold thread per row (<= 512)
-  p.one_tile = (pair_tiles <= pairs && !replay) ? 1 : 0;
+  p.few_tiles = (pair_tiles <= 2 * pairs && !replay) ? 1 : 0;
 
   switch (kind) {
     case K_BF16:

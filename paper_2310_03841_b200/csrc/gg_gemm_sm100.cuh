@@ -64,7 +64,7 @@ struct Params {
   int c_tma;            // 1: C is stored through smem boxes + TMA (needs 16 B aligned C and pitch)
   int sched;            // 0: contiguous tile range per pair, 1: strided (long K)
   int tiny;             // <= 1 tile per pair, <= 4 bands: one launch-wide fold from smem (fewest round trips)
-  int one_tile;         // <= 1 tile per pair: split bands fold from one burst into the idle stages
+  int few_tiles;        // <= 2 tiles per pair: a split band is folded at the kernel end by all threads of the CTA completing it
   int dbg;              // diagnostics only ($GG_DEBUG), 0 in production: 1 skip predicted dot products,
                         // 2 decouple the checksum warps from the stages, 4 skip band folds, 8 skip
                         // observed sums, 16 relaxed (unordered) split-band counts, 32 drop the

@@ -36,6 +36,12 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* addr, int v) {
   asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu_u64(unsigned long long* addr,
+                                                                      unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(addr), "l"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ unsigned long long atom_add_release_gpu_u64(unsigned long long* addr,
                                                                       unsigned long long v) {
   unsigned long long old;

@@ -177,10 +177,11 @@ def test_packed_output_campaign_equals_one_launch_per_fault(dtype):
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.int8])
 @pytest.mark.parametrize("shape", [(1024, 3072, 768), (512, 8192, 256)])
-def test_one_tile_per_pair_launch_burst_fold(dtype, shape):
-    """At most one tile per CTA pair but more than four bands: every band is split
-    and its finisher folds the partials from one burst into the idle stages.  Faults
-    in several bands are flagged exactly, and replay restores the clean bytes."""
+def test_one_tile_per_pair_launch_end_fold(dtype, shape):
+    """At most one tile per CTA pair: every band is split and folded at the end of the
+    kernel by all threads of the CTA completing it (more than four bands), or every row
+    by the launch's last CTA (tiny).  Faults in several bands are flagged exactly, and
+    replay restores the clean bytes."""
     M, N, Kd = shape
     x, w, b, ws, bs = _ops(M, N, Kd, dtype, 41)
     clean, r0 = K.protected_gemm(x, w, b, w_sum=ws, bias_sum=bs, lo=-1e30, hi=1e30)
