@@ -77,11 +77,17 @@ struct Vec<float> {
   }
 };
 
-// CH = 16-byte chunks per lane (D = 32 * CH * Vec::N); one warp per row (the rows in flight
-// hide HBM latency: holding gamma / beta in registers over 4 rows per warp measured 1.7x slower).
+// 256-thread blocks resident per SM for a lane holding `floats` row values (register budget)
+constexpr int ln_min_blocks(int floats) { return floats <= 24 ? 4 : floats <= 32 ? 3 : floats <= 48 ? 2 : 1; }
+
+// CH = 16-byte chunks per lane (D = 32 * CH * Vec::N); one warp per row.  The rows in flight
+// hide HBM latency, and those come from resident warps, so the register budget is capped for
+// four 256-thread blocks per SM at D = 768: the predicted-sum variant otherwise took more than
+// 64 registers, three blocks, and ran 25% slower (two or four rows per warp sharing the affine
+// parameter loads measured slower still).
 template <typename T, int CH, bool PRED>
 // h_out may alias h (in-place residual update): neither is __restrict__.
-__global__ void __launch_bounds__(256) add_layernorm_kernel(const T* h, const T* __restrict__ y, int64_t rows, int D,
+__global__ void __launch_bounds__(256, ln_min_blocks(CH * Vec<T>::N)) add_layernorm_kernel(const T* h, const T* __restrict__ y, int64_t rows, int D,
                                                             const float* __restrict__ gamma,
                                                             const float* __restrict__ beta, float eps, T* h_out,
                                                             T* __restrict__ ln_out, const float* __restrict__ w_pred,
