@@ -168,6 +168,29 @@ GG_API int gg_protected_gemm(const gg_gemm_desc* desc, void* stream);
  * Replaces guard._replay (guard.py:575-604). */
 GG_API int gg_replay_tiles(const gg_gemm_desc* desc, void* stream);
 
+/* Tile localisation by column checksums (north_star kernel (1): e^T A and the
+ * column sums of C; not in the reference, which checks rows only, SPEC.md:497,
+ * and replays the whole layer, guard.py:575-604).  For every 128-row band
+ * holding a row with flags[r] != 0, the column discrepancies
+ *   e[b, n] = (sum_{r in b} X[r, :]) . W[n, :] + rows_b * bias[n] - sum_{r in b} C[r, n]
+ * (int64 for int8 operands, fp64 otherwise) and tile_mask[b * n_tiles + t] = 1
+ * for each 256-column tile t holding a column with e != 0 (int8), or (floats)
+ * a non-finite e or |e| > frac * min over the band's flagged rows with a
+ * finite d of |d[r] - mu|.
+ * X [M, K] (ldx) and W [N, K] (ldw, torch layout) of x_dtype (GG_BF16, GG_F16,
+ * GG_F32, GG_I8); C [M, N] (ldc) of c_dtype (the K1 output type); bias [N] of
+ * bias_dtype or NULL; d the K1 result's d (f64, or i64 for int8).  tile_mask:
+ * ceil(M/128) x ceil(N/256) bytes (zeroed here); col_disc (optional, may be
+ * NULL): ceil(M/128) x N values, written for the flagged bands only.
+ * workspace: gg_locate_workspace_bytes(M, K) bytes of device scratch. */
+GG_API size_t gg_locate_workspace_bytes(int64_t M, int64_t K);
+GG_API int gg_locate_tiles(int32_t x_dtype, const void* X, int64_t M, int64_t K, int64_t ldx,
+                           const void* W, int64_t N, int64_t ldw, const void* bias,
+                           int32_t bias_dtype, int32_t c_dtype, const void* C, int64_t ldc,
+                           const uint8_t* flags, const void* d, double mu, double frac,
+                           uint8_t* tile_mask, void* col_disc, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* K2 — offline weight checksum w_sum[k] = sum_n W[n,k] (ascending n) and
  * bias_sum = sum_n bias[n] in precision chk_prec; bit-exact with
  * guard.offline_checksum (guard.py:142-160, _accumulate_in 135-139).

@@ -38,6 +38,8 @@ EXPORTED_SYMBOLS = (
     "gg_split_tf32x3",
     "gg_offline_checksum",
     "gg_verify_rows",
+    "gg_locate_workspace_bytes",
+    "gg_locate_tiles",
     "gg_flip_bits",
     "gg_gemm_exact",
     "gg_reduce",
@@ -146,6 +148,14 @@ def load(path: Path | None = None):
     lib.gg_verify_rows.argtypes = [
         c_int32, c_void_p, c_int64, c_int64, c_int64, c_int32, c_void_p, c_int64, c_int64, c_int32, c_void_p,
         c_void_p, c_double, c_double, c_double, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+    ]
+    lib.gg_locate_workspace_bytes.restype = ctypes.c_size_t
+    lib.gg_locate_workspace_bytes.argtypes = [c_int64, c_int64]
+    lib.gg_locate_tiles.restype = c_int32
+    lib.gg_locate_tiles.argtypes = [
+        c_int32, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int32,
+        c_void_p, c_int64, c_void_p, c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p, ctypes.c_size_t,
+        c_void_p,
     ]
     lib.gg_flip_bits.restype = c_int32
     lib.gg_flip_bits.argtypes = [c_void_p, c_int32, c_void_p, c_void_p, c_int64, c_void_p]

@@ -25,7 +25,7 @@ INCLUDE = PKG.parent / "include"
 BUILD = PKG / "_build"
 LIB = PKG / "libgemmguard_b200.so"
 
-SOURCES = ["gg_gemm_sm100.cu", "gg_aux.cu", "gg_calib.cu", "gg_toy.cu", "gg_vit.cu", "gg_capi.cu"]
+SOURCES = ["gg_gemm_sm100.cu", "gg_aux.cu", "gg_calib.cu", "gg_toy.cu", "gg_vit.cu", "gg_locate.cu", "gg_capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3",

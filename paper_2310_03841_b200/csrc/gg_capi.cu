@@ -71,6 +71,17 @@ int gg_verify_rows(int32_t x_dtype, const void* X, int64_t M, int64_t K, int64_t
                                 static_cast<cudaStream_t>(stream));
 }
 
+size_t gg_locate_workspace_bytes(int64_t M, int64_t K) { return gg::locate_workspace_bytes(M, K); }
+
+int gg_locate_tiles(int32_t x_dtype, const void* X, int64_t M, int64_t K, int64_t ldx, const void* W, int64_t N,
+                    int64_t ldw, const void* bias, int32_t bias_dtype, int32_t c_dtype, const void* C, int64_t ldc,
+                    const uint8_t* flags, const void* d, double mu, double frac, uint8_t* tile_mask, void* col_disc,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  return gg::launch_locate_tiles(x_dtype, X, M, K, ldx, W, N, ldw, bias, bias_dtype, c_dtype, C, ldc, flags, d, mu,
+                                 frac, tile_mask, col_disc, workspace, workspace_bytes,
+                                 static_cast<cudaStream_t>(stream));
+}
+
 int gg_flip_bits(void* ptr, int32_t elem_bytes, const int64_t* elem_idx, const int32_t* bit_idx, int64_t n,
                  void* stream) {
   return gg::launch_flip_bits(ptr, elem_bytes, elem_idx, bit_idx, n, static_cast<cudaStream_t>(stream));

@@ -69,6 +69,13 @@ int launch_add_layernorm(int dtype, const void* h, const void* y, int64_t rows, 
                          const float* beta, float eps, void* h_out, void* ln_out, const float* w_pred,
                          unsigned long long* pred_out, cudaStream_t s);
 
+// implemented in gg_locate.cu
+size_t locate_workspace_bytes(int64_t M, int64_t K);
+int launch_locate_tiles(int x_dtype, const void* X, int64_t M, int64_t K, int64_t ldx, const void* W, int64_t N,
+                        int64_t ldw, const void* bias, int bias_dtype, int c_dtype, const void* C, int64_t ldc,
+                        const uint8_t* flags, const void* d, double mu, double frac, uint8_t* tile_mask,
+                        void* col_disc, void* workspace, size_t workspace_bytes, cudaStream_t s);
+
 // implemented in gg_gemm_sm100.cu
 size_t protected_gemm_workspace_bytes(int64_t M, int64_t N);
 int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s);

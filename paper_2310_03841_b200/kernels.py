@@ -441,6 +441,119 @@ def replay_tiles(
     return changed
 
 
+BAND_ROWS, TILE_COLS = 128, 256  # K1's row band (one CTA) and column tile (one CTA pair)
+
+
+def locate_tiles(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    bias: torch.Tensor | None,
+    y: torch.Tensor,
+    result: CheckResult,
+    *,
+    mu: float = 0.0,
+    frac: float = 0.5,
+    with_columns: bool = False,
+) -> tuple[torch.Tensor, torch.Tensor | None]:
+    """Column checksums of the flagged bands (gg_locate_tiles): which 256-column tiles of
+    each 128-row band hold the fault its row check flagged.
+
+    Returns (tile_mask [ceil(M/128), ceil(N/256)] uint8, col_disc [ceil(M/128), N] or None):
+    the column discrepancies e^T (X W^T + b) - e^T C of the flagged bands (int64 for int8,
+    fp64 otherwise; zero rows for bands without a flag)."""
+    dev = _require_cuda(x, w, bias, y)
+    _check_gemm_operands(x, w, bias)
+    if x.stride(1) != 1 or w.stride(1) != 1 or y.stride(1) != 1:
+        raise ValueError("locate_tiles: rows must be contiguous")
+    M, K = x.shape
+    N = w.shape[0]
+    mt, nt = (M + BAND_ROWS - 1) // BAND_ROWS, (N + TILE_COLS - 1) // TILE_COLS
+    mask = torch.empty((mt, nt), dtype=torch.uint8, device=dev)
+    integer = x.dtype == torch.int8
+    cols = torch.zeros((mt, N), dtype=torch.int64 if integer else torch.float64, device=dev) if with_columns else None
+    lib = L.load()
+    ws = torch.empty(int(lib.gg_locate_workspace_bytes(M, K)), dtype=torch.uint8, device=dev)
+    L.check(
+        lib.gg_locate_tiles(
+            TORCH_TO_GG[x.dtype], x.data_ptr(), M, K, x.stride(0), w.data_ptr(), N, w.stride(0), _ptr(bias),
+            TORCH_TO_GG[bias.dtype] if bias is not None else 0, TORCH_TO_GG[y.dtype], y.data_ptr(), y.stride(0),
+            result.flags.data_ptr(), result.d.data_ptr(), float(mu), float(frac), mask.data_ptr(), _ptr(cols),
+            ws.data_ptr(), ws.numel(), _stream(dev),
+        ),
+        "gg_locate_tiles",
+    )
+    return mask, cols
+
+
+def replay_located(
+    x: torch.Tensor,
+    w: torch.Tensor,
+    bias: torch.Tensor | None,
+    y: torch.Tensor,
+    result: CheckResult,
+    *,
+    w_sum: torch.Tensor,
+    bias_sum: float | int,
+    mu: float = 0.0,
+    lo: float = 0.0,
+    hi: float = 0.0,
+    f32_mode: str = "3xtf32",
+    w_split: torch.Tensor | None = None,
+    frac: float = 0.5,
+    **band_kw,
+) -> tuple[torch.Tensor, int]:
+    """Tile-granular replay: locate the faulty (band, column tile) pairs by column checksums,
+    recompute only those tiles with the clean weight (K1 on the tile's rows and columns:
+    per-element the same MMA sequence, so a clean tile reproduces its bytes), then re-check
+    the touched bands' rows (gg_verify_rows) and re-derive the launch summary.  A band whose
+    rows still flag (a fault the columns did not place) falls back to K4 on its rows.
+
+    Per-sample statistic and no fused epilogue activation (the check needs the raw output).
+    Returns (changed outputs [1] int32 on the device, tiles recomputed)."""
+    dev = _require_cuda(x, w, bias, y)
+    integer = x.dtype == torch.int8
+    mask, _ = locate_tiles(x, w, bias, y, result, mu=mu, frac=frac)
+    tiles = mask.nonzero().tolist()
+    changed = torch.zeros(1, dtype=torch.int32, device=dev)
+    M, N = x.shape[0], w.shape[0]
+    prec = L.GG_P_I64 if integer else L.GG_P_F64
+    bsum = torch.tensor([bias_sum], dtype=torch.int64 if integer else torch.float64, device=dev)
+    bands = sorted({b for b, _ in tiles})
+    for b, t in tiles:
+        r0, r1 = b * BAND_ROWS, min(M, (b + 1) * BAND_ROWS)
+        c0, c1 = t * TILE_COLS, min(N, (t + 1) * TILE_COLS)
+        view = y[r0:r1, c0:c1]
+        old = view.clone()
+        protected_gemm(x[r0:r1], w[c0:c1], None if bias is None else bias[c0:c1], protect=False, out=view,
+                       f32_mode=f32_mode, w_split=None if w_split is None else w_split[c0:c1])
+        bits = torch.int16 if view.element_size() == 2 else torch.int32
+        changed += (view.view(bits) != old.view(bits)).sum().to(torch.int32)
+    for b in bands:  # re-check the touched bands' rows in the reference order
+        r0, r1 = b * BAND_ROWS, min(M, (b + 1) * BAND_ROWS)
+        rb = verify_rows(x[r0:r1], y[r0:r1], w_sum, bsum, prec, mu=mu, lo=lo, hi=hi)
+        result.d[r0:r1] = rb.d
+        result.flags[r0:r1] = rb.flags
+    keep = result.flags.clone()
+    if bool(keep.any()):  # the columns did not place every fault: K4 on the rows still flagged
+        replay_tiles(x, w, bias, y, keep, result, w_sum=w_sum, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
+                     changed=changed, f32_mode=f32_mode, w_split=w_split, **band_kw)
+    _resummarise(result, mu, integer)  # from the rows (K4's standing band summaries predate the tile fix)
+    return changed, len(tiles)
+
+
+def _resummarise(result: CheckResult, mu: float, integer: bool) -> None:
+    """nflag / triggered / max_disc over every row (the kernels' rule: the largest |d - mu|
+    ignoring NaN, +inf when every d is NaN)."""
+    f = result.flags
+    n = f.to(torch.int32).sum()
+    result.nflag.copy_(n.view(1))
+    result.triggered.copy_((n > 0).to(torch.uint8).view(1))
+    g = result.d.double().abs() if integer else (result.d - mu).abs()
+    g = torch.where(torch.isnan(g), torch.full_like(g, -1.0), g)
+    m = g.max()
+    result.max_disc.copy_(torch.where(m < 0, torch.full_like(m, float("inf")), m).view(1))
+
+
 def offline_checksum(
     w: torch.Tensor, bias: torch.Tensor | None, prec: int, *, layout: int = 0
 ) -> tuple[torch.Tensor, torch.Tensor]:

@@ -295,9 +295,11 @@ class ProtectedSwin(torch.nn.Module):
             if lin.index in stats:
                 lin.set_epsilon(*stats[lin.index].epsilon(confidence))
 
-    def enable_replay(self, layers=None, max_replays: int = 3) -> None:
+    def enable_replay(self, layers=None, max_replays: int = 3, granularity: str = "band") -> None:
+        """Detect-then-replay on `layers` (default: all); granularity as ProtectedViT.enable_replay."""
         self._replay_layers = set(range(self.n_layers)) if layers is None else set(layers)
         self._max_replays = max_replays
+        self._replay_granularity = granularity
         self.replay_events = []
 
     def disable_replay(self) -> None:
@@ -310,7 +312,8 @@ class ProtectedSwin(torch.nn.Module):
         from .errors import GuardError
 
         for attempt in range(1, self._max_replays + 1):
-            n = int(lin.replay(x, y, res.flags.clone(), res).item())
+            n = int(lin.replay(x, y, res.flags.clone(), res,
+                               granularity=getattr(self, "_replay_granularity", "band")).item())
             if n == 0:
                 self.replay_events.append((lin.index, "replay_numerical", attempt))
                 return

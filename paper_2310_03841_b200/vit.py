@@ -169,12 +169,35 @@ class ProtectedLinear(torch.nn.Module):
         return self.aux
 
     def replay(self, x: torch.Tensor, y: torch.Tensor, rows: torch.Tensor, result: K.CheckResult,
-               changed: torch.Tensor | None = None) -> torch.Tensor:
-        """K4 on this layer's last launch: recompute the bands of the flagged rows in place."""
+               changed: torch.Tensor | None = None, granularity: str = "band") -> torch.Tensor:
+        """K4 on this layer's last launch: recompute the bands of the flagged rows in place.
+
+        granularity="tile": locate the faulty 256-column tiles of those bands by column
+        checksums (kernels.locate_tiles) and recompute only them (kernels.replay_located);
+        layers with a fused activation replay whole bands (their check needs the raw output)."""
         kw = self._kw(True)
         kw.pop("protect")
+        if granularity == "tile" and self.act == L.GG_ACT_NONE:
+            ch, _ = K.replay_located(x, self.weight, self.bias, y, result, w_sum=self.w_sum,
+                                     bias_sum=self.bias_sum, mu=kw["mu"], lo=kw["lo"], hi=kw["hi"],
+                                     f32_mode=self.f32_mode, w_split=self.w_split, ws_key=kw["ws_key"],
+                                     pred_in=getattr(self, "last_pred_in", None))
+            if changed is not None:
+                changed += ch
+                return changed
+            return ch
+        if granularity not in ("band", "tile"):
+            raise ValueError(f"unknown replay granularity {granularity!r}")
         return K.replay_tiles(x, self.weight, self.bias, y, rows, result, changed=changed,
                               pred_in=getattr(self, "last_pred_in", None), **kw)
+
+
+def _located(lin: "ProtectedLinear", x: torch.Tensor, y: torch.Tensor, res: K.CheckResult) -> list:
+    """The (128-row band, 256-column tile) pairs column checksums place the flagged faults in."""
+    if lin.act != L.GG_ACT_NONE:
+        return []
+    mask, _ = K.locate_tiles(x, lin.weight, lin.bias, y, res, mu=lin.mu)
+    return [tuple(t) for t in mask.nonzero().tolist()]
 
 
 @dataclass
@@ -397,13 +420,16 @@ class ProtectedViT(torch.nn.Module):
         return bf.logits
 
     # ------------------------------------------------------ detect + replay
-    def enable_replay(self, layers=None, max_replays: int = 3) -> None:
+    def enable_replay(self, layers=None, max_replays: int = 3, granularity: str = "band") -> None:
         """Detect-then-replay (guard._replay, guard.py:575-604) on `layers` (default: all):
         after a protected launch whose check triggered, K4 recomputes only the
-        128-row bands holding flagged rows with the clean weight; the host reads
-        one device scalar per protected layer (the reference checks per layer too)."""
+        128-row bands holding flagged rows with the clean weight (granularity="tile":
+        only the 256-column tiles of those bands that column checksums place the
+        fault in); the host reads one device scalar per protected layer (the
+        reference checks per layer too)."""
         self._replay_layers = set(range(self.cfg.n_layers)) if layers is None else set(layers)
         self._max_replays = max_replays
+        self._replay_granularity = granularity
         self.replay_events = []
 
     def disable_replay(self) -> None:
@@ -416,7 +442,8 @@ class ProtectedViT(torch.nn.Module):
         from .errors import GuardError
 
         for attempt in range(1, self._max_replays + 1):
-            changed = lin.replay(x, y, res.flags.clone(), res)
+            changed = lin.replay(x, y, res.flags.clone(), res,
+                                 granularity=getattr(self, "_replay_granularity", "band"))
             n_changed = int(changed.item())
             if n_changed == 0:  # the recompute reproduced the flagged bytes: numerical, accepted
                 self.replay_events.append((lin.index, "replay_numerical", attempt))
@@ -425,7 +452,7 @@ class ProtectedViT(torch.nn.Module):
                 self.replay_events.append((lin.index, "replay", attempt))
                 return
         raise GuardError(f"layer {lin.index}: replay budget ({self._max_replays}) exhausted; "
-                         "persistent fault suspected")
+                         f"persistent fault suspected in (band, column tile) {_located(lin, x, y, res)}")
 
     # ---------------------------------------------------------- calibration
     @torch.no_grad()
