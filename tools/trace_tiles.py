@@ -18,8 +18,10 @@ y = torch.empty(M, N, dtype=K.default_out_dtype(dt), device='cuda'); res = K.Che
 lib = L.load(); lib.gg_trace_buffer.argtypes = [ctypes.c_void_p]
 TT, EV = 64, 28
 buf = torch.zeros(148 * TT * EV + 4 * 64 * 4, dtype=torch.int64, device='cuda')
-run = (lambda: K.protected_gemm(x, w, b, w_sum=ws, w_aux=aux, bias_sum=bsv, lo=-1e30, hi=1e30, out=y, result=res)) \
-    if protect else (lambda: K.protected_gemm(x, w, b, protect=False, out=y))
+act = int(os.environ.get('ACT', '0'))  # 1: the fused tanh-GELU epilogue
+run = (lambda: K.protected_gemm(x, w, b, w_sum=ws, w_aux=aux, bias_sum=bsv, lo=-1e30, hi=1e30, out=y, result=res,
+                                act=act)) \
+    if protect else (lambda: K.protected_gemm(x, w, b, protect=False, out=y, act=act))
 for _ in range(3): run()
 torch.cuda.synchronize()
 lib.gg_trace_buffer(ctypes.c_void_p(buf.data_ptr()))
