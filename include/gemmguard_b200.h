@@ -142,7 +142,21 @@ typedef struct gg_gemm_desc {
    * from its staged A tiles.  Float kinds only.  With it the kernel's
    * checksum warps do no dot products and hold no pipeline stage. */
   const void* pred_in;
+
+  /* Layout of B: GG_B_NK (0) = [N, K] row-major (torch Linear, K-major: what the
+   * tensor cores read) or GG_B_KN (1) = [K, N] row-major (the reference's Wt,
+   * model.py:43; ldb >= N).  With GG_B_KN the launcher first transposes B into
+   * b_scratch (caller-owned device memory of gg_b_scratch_bytes(ab_kind, N, K)
+   * bytes) on the stream; callers that reuse a weight should transpose it once. */
+  int32_t b_layout;
+  void* b_scratch;
+  size_t b_scratch_bytes;
 } gg_gemm_desc;
+
+enum gg_b_layout { GG_B_NK = 0, GG_B_KN = 1 };
+
+/* Bytes of b_scratch a GG_B_KN launch needs: N rows of K elements padded to 16 bytes. */
+GG_API size_t gg_b_scratch_bytes(int32_t ab_kind, int64_t N, int64_t K);
 
 /* Library identity. */
 GG_API const char* gg_last_error(void);

@@ -22,6 +22,7 @@ GG_F64, GG_F32, GG_F16, GG_BF16, GG_I8, GG_I32, GG_I64, GG_TF32X3 = range(8)
 GG_P_F16, GG_P_F32, GG_P_F64, GG_P_I64 = range(4)
 GG_PER_SAMPLE, GG_BATCH_MEAN = 0, 1
 GG_INJ_OUTPUT, GG_INJ_ACCUMULATOR = 0, 1
+GG_B_NK, GG_B_KN = 0, 1
 GG_INJ_BITFLIP, GG_INJ_SET_VALUE = 0, 1
 GG_ACT_NONE, GG_ACT_GELU_TANH = 0, 1
 GG_OK, GG_EINVAL, GG_ECUDA, GG_EWORKSPACE, GG_EUNSUPPORTED = 0, -1, -2, -3, -4
@@ -31,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "gg_last_error",
     "gg_version",
     "gg_protected_gemm_workspace_bytes",
+    "gg_b_scratch_bytes",
     "gg_protected_gemm",
     "gg_replay_tiles",
     "gg_checksum_aux_bytes",
@@ -99,6 +101,9 @@ class GGGemmDesc(ctypes.Structure):
         ("changed", c_void_p),
         ("epilogue_act", c_int32),
         ("pred_in", c_void_p),
+        ("b_layout", c_int32),
+        ("b_scratch", c_void_p),
+        ("b_scratch_bytes", c_size_t),
     ]
 
 
@@ -149,6 +154,8 @@ def load(path: Path | None = None):
         c_int32, c_void_p, c_int64, c_int64, c_int64, c_int32, c_void_p, c_int64, c_int64, c_int32, c_void_p,
         c_void_p, c_double, c_double, c_double, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
     ]
+    lib.gg_b_scratch_bytes.restype = c_size_t
+    lib.gg_b_scratch_bytes.argtypes = [c_int32, c_int64, c_int64]
     lib.gg_locate_workspace_bytes.restype = ctypes.c_size_t
     lib.gg_locate_workspace_bytes.argtypes = [c_int64, c_int64]
     lib.gg_locate_tiles.restype = c_int32

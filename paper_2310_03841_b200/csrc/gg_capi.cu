@@ -71,6 +71,8 @@ int gg_verify_rows(int32_t x_dtype, const void* X, int64_t M, int64_t K, int64_t
                                 static_cast<cudaStream_t>(stream));
 }
 
+size_t gg_b_scratch_bytes(int32_t ab_kind, int64_t N, int64_t K) { return gg::b_scratch_bytes(ab_kind, N, K); }
+
 size_t gg_locate_workspace_bytes(int64_t M, int64_t K) { return gg::locate_workspace_bytes(M, K); }
 
 int gg_locate_tiles(int32_t x_dtype, const void* X, int64_t M, int64_t K, int64_t ldx, const void* W, int64_t N,

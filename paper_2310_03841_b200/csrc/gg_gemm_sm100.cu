@@ -278,8 +278,67 @@ int dispatch_protect(bool protect, int act, const CUtensorMap& ta, const CUtenso
 
 size_t protected_gemm_workspace_bytes(int64_t M, int64_t N) { return ws_layout(M, N).total; }
 
+namespace {
+// [K, N] (ld = ldb) -> [N, Kp] row-major through 32 x 32 shared tiles (coalesced both sides)
+template <typename E>
+__global__ void transpose_kn_kernel(const E* __restrict__ src, int64_t K, int64_t N, int64_t ldb, E* __restrict__ dst,
+                                    int64_t ldd) {
+  __shared__ E tile[32][33];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.y) * 32, n0 = static_cast<int64_t>(blockIdx.x) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t k = k0 + i, n = n0 + threadIdx.x;
+    if (k < K && n < N) tile[i][threadIdx.x] = src[k * ldb + n];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < K) dst[n * ldd + k] = tile[threadIdx.x][i];
+  }
+}
+
+int64_t padded_k(int elem, int64_t K) {
+  const int64_t step = 16 / elem;
+  return (K + step - 1) / step * step;
+}
+}  // namespace
+
+size_t b_scratch_bytes(int ab_kind, int64_t N, int64_t K) {
+  const int elem = ab_kind == GG_F32 ? 4 : ab_kind == GG_I8 ? 1 : 2;
+  return static_cast<size_t>(N) * static_cast<size_t>(padded_k(elem, K)) * static_cast<size_t>(elem);
+}
+
 int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   if (d == nullptr) return fail(GG_EINVAL, "protected_gemm: null descriptor");
+  if (d->b_layout == GG_B_KN) {
+    // the reference's Wt [K, N]: transposed into the caller's scratch, then the K-major launch
+    const int elem = d->ab_kind == GG_F32 ? 4 : d->ab_kind == GG_I8 ? 1 : 2;
+    if (d->ab_kind != GG_BF16 && d->ab_kind != GG_F16 && d->ab_kind != GG_F32 && d->ab_kind != GG_I8)
+      return fail(GG_EUNSUPPORTED, "protected_gemm: ab_kind must be GG_BF16, GG_F16, GG_F32 or GG_I8");
+    if (d->N < 1 || d->K < 1) return fail(GG_EINVAL, "gemm dims mismatch: M, N, K must be positive");
+    if (d->B == nullptr || d->b_scratch == nullptr) return fail(GG_EINVAL, "protected_gemm: GG_B_KN needs B and b_scratch");
+    if (d->ldb < d->N) return fail(GG_EINVAL, "protected_gemm: GG_B_KN needs ldb >= N");
+    if (d->b_scratch_bytes < b_scratch_bytes(d->ab_kind, d->N, d->K))
+      return fail(GG_EWORKSPACE, "protected_gemm: b_scratch too small (gg_b_scratch_bytes)");
+    if (reinterpret_cast<uintptr_t>(d->b_scratch) & 15) return fail(GG_EINVAL, "protected_gemm: b_scratch must be 16-byte aligned");
+    const int64_t kp = padded_k(elem, d->K);
+    const dim3 grid(static_cast<unsigned>((d->N + 31) / 32), static_cast<unsigned>((d->K + 31) / 32)), block(32, 8);
+    if (grid.y > 65535) return fail(GG_EUNSUPPORTED, "protected_gemm: GG_B_KN with K beyond 2^21");
+    switch (elem) {
+      case 1: transpose_kn_kernel<uint8_t><<<grid, block, 0, s>>>(static_cast<const uint8_t*>(d->B), d->K, d->N, d->ldb,
+                                                                  static_cast<uint8_t*>(d->b_scratch), kp); break;
+      case 2: transpose_kn_kernel<uint16_t><<<grid, block, 0, s>>>(static_cast<const uint16_t*>(d->B), d->K, d->N, d->ldb,
+                                                                   static_cast<uint16_t*>(d->b_scratch), kp); break;
+      default: transpose_kn_kernel<uint32_t><<<grid, block, 0, s>>>(static_cast<const uint32_t*>(d->B), d->K, d->N, d->ldb,
+                                                                    static_cast<uint32_t*>(d->b_scratch), kp); break;
+    }
+    if (const int rc = check_launch("protected_gemm (B transpose)")) return rc;
+    gg_gemm_desc nk = *d;
+    nk.B = d->b_scratch;
+    nk.ldb = kp;
+    nk.b_layout = GG_B_NK;
+    return launch_protected_gemm(&nk, replay, s);
+  }
+  if (d->b_layout != GG_B_NK) return fail(GG_EINVAL, "protected_gemm: b_layout must be GG_B_NK or GG_B_KN");
   if (d->M < 1 || d->N < 1 || d->K < 1) return fail(GG_EINVAL, "gemm dims mismatch: M, N, K must be positive");
   if (d->M > (int64_t(1) << 30) || d->N > (int64_t(1) << 30) || d->K > (int64_t(1) << 30))
     return fail(GG_EINVAL, "protected_gemm: dims beyond 2^30");

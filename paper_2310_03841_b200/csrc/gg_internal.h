@@ -78,6 +78,7 @@ int launch_locate_tiles(int x_dtype, const void* X, int64_t M, int64_t K, int64_
 
 // implemented in gg_gemm_sm100.cu
 size_t protected_gemm_workspace_bytes(int64_t M, int64_t N);
+size_t b_scratch_bytes(int ab_kind, int64_t N, int64_t K);
 int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s);
 
 }  // namespace gg

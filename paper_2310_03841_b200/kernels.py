@@ -353,6 +353,61 @@ def protected_gemm(
     return y, (result if protect else None)
 
 
+def protected_gemm_wt(
+    x: torch.Tensor,
+    wt: torch.Tensor,
+    bias: torch.Tensor | None = None,
+    *,
+    protect: bool = True,
+    w_sum: torch.Tensor | None = None,
+    w_aux: torch.Tensor | None = None,
+    bias_sum: float | int = 0,
+    mu: float = 0.0,
+    lo: float = 0.0,
+    hi: float = 0.0,
+    statistic: int = L.GG_PER_SAMPLE,
+    out: torch.Tensor | None = None,
+    result: CheckResult | None = None,
+    ws_key=None,
+    f32_mode: str = "tf32",
+) -> tuple[torch.Tensor, CheckResult | None]:
+    """K1 on the reference's weight layout Wt [K, N] (numerics.gemm's `Wt`, model.py:43):
+    the descriptor's b_layout = GG_B_KN, so the launcher transposes Wt into a scratch buffer
+    and runs the K-major kernel -- results identical to protected_gemm(x, Wt.T.contiguous()).
+    fp32 operands take the single-pass tf32 engine here (3xTF32 splits a [N, K] weight)."""
+    dev = _require_cuda(x, wt, bias)
+    if x.dim() != 2 or wt.dim() != 2 or x.shape[1] != wt.shape[0]:
+        raise ValueError(f"gemm dims mismatch: X is {tuple(x.shape)}, Wt is {tuple(wt.shape)} ([K, N])")
+    _check_gemm_operands(x, wt.t(), bias)
+    if x.dtype == torch.float32 and _f32_mode(f32_mode) != "tf32":
+        raise ValueError("protected_gemm_wt: fp32 operands need f32_mode='tf32' (3xTF32 splits [N, K] weights)")
+    if wt.stride(1) != 1:
+        raise ValueError("protected_gemm_wt: Wt rows must be contiguous")
+    xs = _pad_k(x)
+    M, N = x.shape[0], wt.shape[1]
+    lib = L.load()
+    scratch = torch.empty(int(lib.gg_b_scratch_bytes(TORCH_TO_GG[x.dtype], N, x.shape[1])), dtype=torch.uint8,
+                          device=dev)
+    y = out if out is not None else torch.empty((M, N), dtype=default_out_dtype(x.dtype), device=dev)
+    if protect:
+        if w_sum is None:
+            raise ValueError("protect=True needs the offline checksum w_sum")
+        if w_aux is None:
+            w_aux = checksum_aux(w_sum, x.dtype, f32_mode)
+        result = result or CheckResult.empty(M, x.dtype == torch.int8, dev)
+        ws = workspace(M, N, dev, ws_key)
+    else:
+        ws = None
+    desc = build_desc(xs, wt.t(), y, bias, protect=protect, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu,
+                      lo=lo, hi=hi, statistic=statistic, result=result, ws=ws)
+    desc.ldb = wt.stride(0)
+    desc.b_layout = L.GG_B_KN
+    desc.b_scratch = scratch.data_ptr()
+    desc.b_scratch_bytes = scratch.numel()
+    L.check(lib.gg_protected_gemm(ctypes.byref(desc), _stream(dev)), "gg_protected_gemm")
+    return y, (result if protect else None)
+
+
 def packed_output_campaign(
     x: torch.Tensor,
     w: torch.Tensor,

@@ -441,3 +441,4 @@ def test_albt_loads_into_device_memory(name):
         chk = offline_checksum(ly, p)
         assert dw.w_sum[ly.index].cpu().numpy().tobytes() == chk.w_sum.tobytes()
         assert dw.bias_sum[ly.index] == chk.bias_sum
+
