@@ -62,7 +62,8 @@ enum gg_inj_mode { GG_INJ_BITFLIP = 0, GG_INJ_SET_VALUE = 1 }; /* injector.py:49
  * the check covers the raw (rounded, bias-included) GEMM output exactly as
  * guard.py:10-11 / model.py:367-368, the activation of that value is what is
  * stored (model.finish_layer_output's GELU, model.py:281-285, 318-319). */
-enum gg_epilogue_act { GG_ACT_NONE = 0, GG_ACT_GELU_TANH = 1 /* bf16 / fp16 outputs */ };
+enum gg_epilogue_act { GG_ACT_NONE = 0, GG_ACT_GELU_TANH = 1 /* bf16 / fp16 outputs */,
+                       GG_ACT_RELU = 2 /* int8 requantised outputs (c_dtype GG_I8) */ };
 
 enum gg_error {
   GG_OK = 0,
@@ -151,6 +152,14 @@ typedef struct gg_gemm_desc {
   int32_t b_layout;
   void* b_scratch;
   size_t b_scratch_bytes;
+
+  /* Int8 operands with c_dtype = GG_I8: the stored output is the requantised hidden state
+   * h = clip(((relu ? max(y, 0) : y) + 2^(s-1)) >> s, -128, 127) of the int32 GEMM output y
+   * (int32 wrap-around, arithmetic shift: model.finish_layer_output's requantisation,
+   * model.py:312-316), s = requant_shift in [1, 30], relu with epilogue_act = GG_ACT_RELU.
+   * The check runs on y (guard.py:170: the GEMM output, before the layer glue); C is [M, N]
+   * int8 (ldc in bytes). */
+  int32_t requant_shift;
 } gg_gemm_desc;
 
 enum gg_b_layout { GG_B_NK = 0, GG_B_KN = 1 };

@@ -369,7 +369,13 @@ __device__ __forceinline__ float add_f32_h16(float acc, uint32_t w, bool high) {
 // Write the 32 output encodings of this thread's box row into the swizzled staging box.
 template <int OUT>
 __device__ __forceinline__ void stage_row(uint32_t box, int lane, const uint32_t (&o)[32]) {
-  if constexpr (OUT == O_BF16 || OUT == O_F16) {
+  if constexpr (OUT == O_I8) {
+    const uint32_t row = box + static_cast<uint32_t>(lane * 32);  // SWIZZLE_32B: chunk ^= (row >> 2) & 1
+    const int sw = (lane >> 2) & 1;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)  // o[] holds four bytes per word
+      sts128(row + static_cast<uint32_t>((c ^ sw) << 4), o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+  } else if constexpr (OUT == O_BF16 || OUT == O_F16) {
     const uint32_t row = box + static_cast<uint32_t>(lane * 64);  // SWIZZLE_64B: chunk ^= (row >> 1) & 3
     const int sw = (lane >> 1) & 3;
 #pragma unroll
@@ -387,7 +393,27 @@ __device__ __forceinline__ void stage_row(uint32_t box, int lane, const uint32_t
 // Epilogue activations applied to the stored encoding AFTER the observed row sum
 // (the check runs on the raw, rounded GEMM output: guard.py:10-11, model.py:367-368,
 // SURVEY §8(a) a4 (ii)); the activated value is rounded to the output type again.
-enum : int { ACT_NONE = 0, ACT_GELU_TANH = 1 };
+enum : int { ACT_NONE = 0, ACT_GELU_TANH = 1, ACT_RELU = 2 };
+
+// model.finish_layer_output's requantisation of an int32 output (model.py:312-316):
+// clip(((relu ? max(y, 0) : y) + 2^(s-1)) >> s, -128, 127), int32 wrap-around as NumPy
+template <bool RELU>
+__device__ __forceinline__ int requant_pre(uint32_t y, int shift) {  // before the saturation
+  int h = static_cast<int>(y);
+  if constexpr (RELU) h = max(h, 0);
+  h = static_cast<int>(static_cast<unsigned>(h) + (1u << (shift - 1)));
+  return h >> shift;
+}
+// four outputs requantised and packed (byte i = output i), saturation by cvt.pack.sat (I2IP)
+template <bool RELU>
+__device__ __forceinline__ uint32_t requant8x4(const uint32_t* y, int shift) {
+  const int a0 = requant_pre<RELU>(y[0], shift), a1 = requant_pre<RELU>(y[1], shift);
+  const int a2 = requant_pre<RELU>(y[2], shift), a3 = requant_pre<RELU>(y[3], shift);
+  uint32_t hi, w;
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(a3), "r"(a2));
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(w) : "r"(a1), "r"(a0), "r"(hi));
+  return w;
+}
 
 // tanh-GELU of an fp32 pair (model._gelu: 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))));
 // tanh on the MUFU pipe (tanh.approx.f32, |rel err| ~2^-11, below bf16 output rounding)
@@ -1112,11 +1138,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             o[i] = (OUT == O_BF16) ? pack_bf16x2(g.x, g.y) : pack_f16x2(g.x, g.y);
           }
         }
+        if constexpr (OUT == O_I8) {  // the checked int32 outputs requantised, four per word in o[0..7]
+          uint32_t h8[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) h8[v] = requant8x4<ACT == ACT_RELU>(o + 4 * v, p.requant_shift);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) o[v] = h8[v];
+        }
+        constexpr bool BOX2 = OUT16 || OUT == O_I8;  // boxes of <= 2 KB: two in flight per warp
         if (c_tma) {
           // coalesced store: this warp's 32 rows x 32 columns through a swizzled smem box + TMA
-          uint8_t* boxp = smC + e * CST_BYTES + (OUT16 ? cbuf * 2048 : 0);
+          uint8_t* boxp = smC + e * CST_BYTES + (BOX2 ? cbuf * 2048 : 0);
           if (lane == 0) {
-            if constexpr (OUT16) bulk_wait_read<1>();  // the box written two chunks ago has been read
+            if constexpr (BOX2) bulk_wait_read<1>();  // the box written two chunks ago has been read
             else bulk_wait_read<0>();
           }
           __syncwarp();
@@ -1127,9 +1161,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             tma_store_2d(&tmC, boxp, col0, row0 + 32 * eg);
             bulk_commit();
           }
-          if constexpr (OUT16) cbuf ^= 1;
+          if constexpr (BOX2) cbuf ^= 1;
           GG_LAP(tr_st);
         } else if (row_ok) {
+          if constexpr (OUT == O_I8) {  // 32 requantised bytes of this row per chunk
+            const uint32_t* h8 = o;
+            uint8_t* cb = static_cast<uint8_t*>(p.C) + static_cast<long long>(row) * p.ldc + col0;
+            if (full && (reinterpret_cast<uintptr_t>(cb) & 15) == 0) {
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                uint4* dst = reinterpret_cast<uint4*>(cb) + v;
+                if (p.replay) {
+                  const uint4 old = *dst;
+                  const uint32_t ow[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+                  for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int bq = 0; bq < 4; ++bq) changed += (((ow[q] ^ h8[4 * v + q]) >> (8 * bq)) & 0xFFu) != 0;
+                }
+                *dst = make_uint4(h8[4 * v], h8[4 * v + 1], h8[4 * v + 2], h8[4 * v + 3]);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (col0 + j >= p.N) continue;
+                const uint8_t e = static_cast<uint8_t>(h8[j >> 2] >> (8 * (j & 3)));
+                if (p.replay) changed += cb[j] != e ? 1 : 0;
+                cb[j] = e;
+              }
+            }
+            continue;
+          }
           const long long base = static_cast<long long>(row) * p.ldc + col0;
           constexpr int WORDS = OUT16 ? 16 : 32;  // 32-bit words of this row's 32 outputs
           uint32_t* cw = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(p.C) + base * (OUT16 ? 2 : 4));

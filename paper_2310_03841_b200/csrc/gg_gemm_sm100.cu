@@ -74,7 +74,7 @@ int make_output_map(CUtensorMap* map, CUtensorMapDataType dt, int elem, void* pt
   cuuint32_t box[2] = {static_cast<cuuint32_t>(pair::CBOX), static_cast<cuuint32_t>(pair::CBOX)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dt, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   elem == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   elem == 1 ? CU_TENSOR_MAP_SWIZZLE_32B : elem == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(GG_ECUDA, "cuTensorMapEncodeTiled (C) failed (code " + std::to_string(int(r)) + ")");
   return 0;
@@ -266,7 +266,13 @@ int dispatch_protect(bool protect, int act, const CUtensorMap& ta, const CUtenso
       return protect ? launch_pair_instance<KIND, OUT, true, false, pair::ACT_GELU_TANH>(ta, tb, tc, p, grid, s)
                      : launch_pair_instance<KIND, OUT, false, false, pair::ACT_GELU_TANH>(ta, tb, tc, p, grid, s);
   }
-  if (act != GG_ACT_NONE) return fail(GG_EUNSUPPORTED, "protected_gemm: epilogue activation needs bf16 or fp16 outputs");
+  if constexpr (OUT == O_I8) {
+    if (act == GG_ACT_RELU)
+      return protect ? launch_pair_instance<KIND, OUT, true, false, pair::ACT_RELU>(ta, tb, tc, p, grid, s)
+                     : launch_pair_instance<KIND, OUT, false, false, pair::ACT_RELU>(ta, tb, tc, p, grid, s);
+  }
+  if (act != GG_ACT_NONE)
+    return fail(GG_EUNSUPPORTED, "protected_gemm: GELU needs bf16 / fp16 outputs, ReLU requantised int8 outputs");
   if (!protect) return launch_pair_instance<KIND, OUT, false>(ta, tb, tc, p, grid, s);
   if constexpr (KIND == K_TF32) {  // claimed split-band folds (see the kernel)
     if (!p.few_tiles && !p.tiny && p.n_tiles >= 8) return launch_pair_instance<KIND, OUT, true, true>(ta, tb, tc, p, grid, s);
@@ -357,10 +363,14 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
     case GG_F16: out = O_F16; break;
     case GG_F32: out = O_F32; break;
     case GG_I32: out = O_I32; break;
+    case GG_I8: out = O_I8; break;
     default: return fail(GG_EUNSUPPORTED, "protected_gemm: unsupported c_dtype");
   }
   const bool int_kind = kind == K_I8;
-  if (int_kind != (out == O_I32)) return fail(GG_EINVAL, "protected_gemm: int8 operands produce int32 outputs only");
+  if (int_kind != (out == O_I32 || out == O_I8))
+    return fail(GG_EINVAL, "protected_gemm: int8 operands produce int32 (or requantised int8) outputs only");
+  if (out == O_I8 && (d->requant_shift < 1 || d->requant_shift > 30))
+    return fail(GG_EINVAL, "protected_gemm: int8 outputs need a requant shift in [1, 30]");
   if (kind == K_BF16 && out == O_F16) return fail(GG_EUNSUPPORTED, "protected_gemm: bf16 -> f16 output not built");
   if (kind == K_F16 && out == O_BF16) return fail(GG_EUNSUPPORTED, "protected_gemm: f16 -> bf16 output not built");
   if (kind == K_TF32 && out != O_F32) return fail(GG_EUNSUPPORTED, "protected_gemm: tf32 produces f32 outputs only");
@@ -400,10 +410,11 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   rc = make_operand_map(&tb, tdt, elem, d->B, d->K, d->N, d->ldb * elem, pair::BN / 2);
   if (rc) return rc;
   // C through the TMA-store epilogue when the pointer and pitch allow it
-  const int out_elem = (out == O_BF16 || out == O_F16) ? 2 : 4;
+  const int out_elem = (out == O_BF16 || out == O_F16) ? 2 : out == O_I8 ? 1 : 4;
   const CUtensorMapDataType cdt = out == O_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                   : out == O_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                   : out == O_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                  : out == O_I8  ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                                  : CU_TENSOR_MAP_DATA_TYPE_INT32;
   CUtensorMap tc;
   std::memset(&tc, 0, sizeof(tc));
@@ -423,6 +434,7 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.C = d->C;
   p.ldc = d->ldc;
   p.c_tma = c_tma;
+  p.requant_shift = d->requant_shift;
 #ifdef GG_DIAGNOSTICS
   if (std::getenv("GG_NO_CTMA")) p.c_tma = 0;  // diagnostics: direct vector stores from registers
 #endif
@@ -518,7 +530,8 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
       rc = dispatch_protect<K_TF32, O_F32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
       break;
     default:
-      rc = dispatch_protect<K_I8, O_I32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
+      rc = out == O_I32 ? dispatch_protect<K_I8, O_I32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s)
+                        : dispatch_protect<K_I8, O_I8>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
   }
   if (rc == 0 && batch_mean)
     rc = launch_batch_mean_finish(d->M, d->mu, d->lo, d->hi, static_cast<const double*>(d->d), d->flags, d->max_disc,

@@ -20,7 +20,7 @@ constexpr int BN = 256;  // N of one tile
 // operand kinds (template KIND)
 enum : int { K_BF16 = 0, K_F16 = 1, K_TF32 = 2, K_I8 = 3 };
 // output kinds (template OUT)
-enum : int { O_BF16 = 0, O_F16 = 1, O_F32 = 2, O_I32 = 3 };
+enum : int { O_BF16 = 0, O_F16 = 1, O_F32 = 2, O_I32 = 3, O_I8 = 4 /* int32 GEMM output, stored requantised */ };
 
 struct Workspace {
   unsigned long long* summary;  // [2] {done bands << 32 | flagged rows, max gap key}: one 128-bit CAS per band
@@ -73,6 +73,7 @@ struct Params {
                         // launch-summary atomics,
                         // 1024 / 2048 force the contiguous / strided schedule
   const void* pred_in;  // [M] predicted row sums (fp32 (hi, lo) pairs) supplied by X's producer, or null
+  int requant_shift;    // O_I8: the stored output's requantisation shift
   int replay;           // 1: only active bands, compare against old C
   int* changed;
   Workspace ws;
@@ -265,7 +266,7 @@ __device__ __forceinline__ double out_bits_to_f64(uint32_t b) {
 // accumulator (+bias) -> stored encoding, round to nearest even
 template <int OUT>
 __device__ __forceinline__ uint32_t acc_to_out_bits(uint32_t acc, uint32_t bias_bits) {
-  if constexpr (OUT == O_I32) {
+  if constexpr (OUT == O_I32 || OUT == O_I8) {
     return acc + bias_bits;  // int32 wrap-around, numerics.py:269-272
   } else {
     const float v = __uint_as_float(acc) + __uint_as_float(bias_bits);

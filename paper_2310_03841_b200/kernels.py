@@ -155,6 +155,7 @@ def build_desc(
     changed: torch.Tensor | None = None,
     act: int = L.GG_ACT_NONE,
     pred_in: torch.Tensor | None = None,
+    requant_shift: int = 0,
 ) -> L.GGGemmDesc:
     M, K = x.shape
     N = w.shape[0]
@@ -191,6 +192,7 @@ def build_desc(
     d.changed = _ptr(changed)
     d.epilogue_act = int(act)
     d.pred_in = _ptr(pred_in) if protect else None
+    d.requant_shift = int(requant_shift)
     return d
 
 
@@ -316,6 +318,7 @@ def protected_gemm(
     w_split: torch.Tensor | None = None,
     act: int = L.GG_ACT_NONE,
     pred_in: torch.Tensor | None = None,
+    requant_shift: int = 0,
 ) -> tuple[torch.Tensor, CheckResult | None]:
     """K1: y = x @ w.T + bias with the fused checksum check (one launch).
 
@@ -325,6 +328,9 @@ def protected_gemm(
     act=GG_ACT_GELU_TANH stores GELU(y) (16-bit outputs) after the check of y.
     pred_in [M] (uint64 fp32 (hi, lo) pairs): the predicted row sums x . w_sum
     computed by x's producer (add_layernorm's pred_out); K1 then skips its own.
+    int8 operands with out_dtype=torch.int8 and requant_shift s store the requantised hidden
+    state clip(((relu ? max(y, 0) : y) + 2^(s-1)) >> s, -128, 127) of the checked int32 y
+    (act=GG_ACT_RELU for the relu; model.finish_layer_output's elementwise part).
     Returns (y, CheckResult or None when protect=False).
     """
     dev = _require_cuda(x, w, bias)
@@ -348,7 +354,7 @@ def protected_gemm(
         inj_dev, n_inj = None, 0
     desc = build_desc(x, w, y, bias, protect=protect, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo,
                       hi=hi, statistic=statistic, result=result, inj_dev=inj_dev, n_inj=n_inj, ws=ws, act=act,
-                      pred_in=_check_pred(pred_in, M))
+                      pred_in=_check_pred(pred_in, M), requant_shift=requant_shift)
     L.check(L.load().gg_protected_gemm(ctypes.byref(desc), _stream(dev)), "gg_protected_gemm")
     return y, (result if protect else None)
 
@@ -476,6 +482,7 @@ def replay_tiles(
     w_split: torch.Tensor | None = None,
     act: int = L.GG_ACT_NONE,
     pred_in: torch.Tensor | None = None,
+    requant_shift: int = 0,
 ) -> torch.Tensor:
     """K4: recompute only the M-bands holding a flagged row, in place in y.
 
@@ -491,7 +498,7 @@ def replay_tiles(
     ws = workspace(M, N, dev, ws_key)
     desc = build_desc(x, w, y, bias, protect=True, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
                       statistic=statistic, result=result, ws=ws, replay_rows=replay_rows, changed=changed, act=act,
-                      pred_in=_check_pred(pred_in, M))
+                      pred_in=_check_pred(pred_in, M), requant_shift=requant_shift)
     L.check(L.load().gg_replay_tiles(ctypes.byref(desc), _stream(dev)), "gg_replay_tiles")
     return changed
 

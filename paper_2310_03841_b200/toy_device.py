@@ -97,18 +97,27 @@ def forward_batch(model: ModelGraph, inputs: Sequence[Matrix2D], labels: Sequenc
         head = layer.kind == "head"
         xin = h.view(B, T, -1)[:, 0, :].contiguous() if head else h
         inj = injections.get(layer.index) if injections else None
+        # elementwise glue (relu + requantisation) fused into K1's epilogue: the check runs on the
+        # int32 output, the int8 hidden state is what is stored; qkv's head mixing and the range
+        # profile (which needs the int32 output) keep the separate gg_int_finish pass
+        fuse = not head and layer.kind != "qkv" and ranges is None
+        rq = dict(out_dtype=torch.int8, requant_shift=_requant_shift(layer.in_dim),
+                  act=L.GG_ACT_RELU if layer.activation == "relu" else L.GG_ACT_NONE) if fuse else {}
         if protect:
             if chks is not None and layer.index in chks:  # the caller's offline checksums (guard.WeightChecksum)
                 ws, bs = chks[layer.index].w_sum_device(), int(chks[layer.index].bias_sum)
             else:
                 ws, bs = _checksum(layer, ent.w_nk, bias)
-            y, res = K.protected_gemm(xin, ent.w_nk, bias, w_sum=ws, bias_sum=bs, lo=0, hi=0, injections=inj)
+            y, res = K.protected_gemm(xin, ent.w_nk, bias, w_sum=ws, bias_sum=bs, lo=0, hi=0, injections=inj, **rq)
             rows = res.flags.view(B, -1) if not head else res.flags.view(B, 1)
             flags[layer.index] = rows.bool().any(dim=1)
             nrows[layer.index] = rows.to(torch.int32).sum(dim=1)
             maxd[layer.index] = res.d.view(B, -1).abs().max(dim=1).values
         else:
-            y, _ = K.protected_gemm(xin, ent.w_nk, bias, protect=False, injections=inj)
+            y, _ = K.protected_gemm(xin, ent.w_nk, bias, protect=False, injections=inj, **rq)
+        if fuse:
+            h = y
+            continue
         if ranges is not None:
             ranges.setdefault(layer.index, RunningRange(dev)).update(y)
         if head:
