@@ -182,6 +182,24 @@ def _flip16(bits: torch.Tensor, bit: torch.Tensor) -> torch.Tensor:
     return (((v + 32768) & 0xFFFF) - 32768).to(torch.int16)
 
 
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _uniform(seed: int, layer: int, k: np.ndarray, attempt: np.ndarray, draw: int) -> np.ndarray:
+    """U[0, 1) as a function of (seed, layer, trial k, attempt, draw index): a SplitMix64
+    finaliser over a mix of the counters (partition- and order-independent, vectorised)."""
+    with np.errstate(over="ignore"):
+        x = (np.uint64(seed & 0xFFFFFFFFFFFFFFFF) * np.uint64(0x9E3779B97F4A7C15)
+             ^ np.uint64(layer) * np.uint64(0xC2B2AE3D27D4EB4F)
+             ^ k * np.uint64(0x165667B19E3779F9) ^ attempt * np.uint64(0xD6E8FEB86659FD93)
+             ^ np.uint64(draw) * np.uint64(0xFF51AFD7ED558CCD))
+        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
 class ViTCampaign:
     """Output bit-flip campaign over the protected layers of a `ProtectedViT`.
 
@@ -198,6 +216,11 @@ class ViTCampaign:
         self.keep_records = keep_records
         self.fields = BF16_FIELDS[model.dtype]
         self.cache: dict = {}
+        # the next block's sampling (clean output of its layer, retry gathers) runs on a side
+        # stream while the previous block's suffix forward occupies the main one: its host
+        # draws overlap the device work instead of waiting behind it
+        self._side = torch.cuda.Stream(self.dev)
+        self._y_layer, self._y = None, None
         with torch.no_grad():
             logits = model.forward(images, protect=True, cache=self.cache)
             self.clean_pred = logits.float().argmax(dim=1).clone()
@@ -214,6 +237,7 @@ class ViTCampaign:
                 rr.update(y)
                 lo, hi, _ = rr.bounds()
                 self.ranges[i] = (lo, hi)
+        self._side.wait_stream(torch.cuda.current_stream(self.dev))  # the cache is read-only from here
 
     # ------------------------------------------------------------ helpers
     def _image_flags(self, i: int) -> torch.Tensor:
@@ -231,9 +255,13 @@ class ViTCampaign:
     # ------------------------------------------------------------ sampling
     def _sample(self, layer: int, ks: np.ndarray, y: torch.Tensor):
         """Element / bit (or value) of each trial k (image k % G) by the reference's retry
-        rules (injector.py:131-210); elem -1 = skipped.  Bit modes flip a bit of the
-        stored encoding; "random_value" draws uniform(lo, hi) and stores it rounded
-        to the output type.  Returns (elem, bit (-1 for value modes), mode index, value)."""
+        rules (injector.py:131-210: element, mode, then bit or value; no-op and range
+        rejection; at most 64 attempts); elem -1 = skipped.  The draws are counter-based
+        (`_uniform` of (seed, layer, k, attempt, draw)), vectorised over the block's trials
+        and four attempts per round; the no-op / range tests run on the device.  Bit modes
+        flip a bit of the stored encoding; "random_value" draws uniform(lo, hi) and stores
+        it rounded to the output type.  Returns (elem, bit (-1 for value modes), mode
+        index, value)."""
         rows = self.model.rows_per_image(layer)
         N = y.shape[1]
         n_elem = rows * N
@@ -243,7 +271,6 @@ class ViTCampaign:
         for m in self.modes:
             if m not in spans and m != "random_value":
                 raise ValueError(f"campaign mode {m!r} is not supported on the device engine")
-        rngs = [np.random.default_rng(np.random.SeedSequence((self.seed, layer, int(k)))) for k in ks]
         n = len(ks)
         elem = np.full(n, -1, dtype=np.int64)
         bit = np.full(n, -1, dtype=np.int64)
@@ -255,23 +282,22 @@ class ViTCampaign:
         wide = y.element_size() == 2
         ybits = y.view(torch.int16) if wide else y.view(torch.int32)
         tries = 0
+        span_lo = np.array([spans[m][0] if m in spans else 0 for m in self.modes], dtype=np.int64)
+        span_w = np.array([spans[m][1] - spans[m][0] if m in spans else 0 for m in self.modes], dtype=np.int64)
+        is_val = np.array([m == "random_value" for m in self.modes])
         while len(pending) and tries < MAX_RETRIES:
             r = min(ROUND, MAX_RETRIES - tries)
-            ce = np.zeros((len(pending), r), dtype=np.int64)
-            cb = np.full((len(pending), r), -1, dtype=np.int64)
-            cm = np.zeros((len(pending), r), dtype=np.int64)
-            cv = np.zeros((len(pending), r), dtype=np.float64)
-            for j, t in enumerate(pending):
-                g = rngs[t]
-                for a in range(r):  # draw order of injector.py:169-186: element, mode, bit | value
-                    ce[j, a] = int(g.integers(n_elem))
-                    cm[j, a] = int(g.integers(len(self.modes)))
-                    mode = self.modes[cm[j, a]]
-                    if mode == "random_value":
-                        cv[j, a] = float(g.uniform(lo, hi))
-                    else:
-                        b0, b1 = spans[mode]
-                        cb[j, a] = int(g.integers(b0, b1))
+            # counter-based draws, vectorised over (trial, attempt): element, mode, then bit or value
+            # -- the draw order of injector.py:169-186, each a function of (seed, layer, k, attempt)
+            kk = ks[pending][:, None].astype(np.uint64)
+            att = (tries + np.arange(r, dtype=np.uint64))[None, :]
+            ce = np.minimum((_uniform(self.seed, layer, kk, att, 0) * n_elem).astype(np.int64), n_elem - 1)
+            cm = np.minimum((_uniform(self.seed, layer, kk, att, 1) * len(self.modes)).astype(np.int64),
+                            len(self.modes) - 1)
+            u2 = _uniform(self.seed, layer, kk, att, 2)
+            cb = np.where(is_val[cm], -1, span_lo[cm] + np.minimum((u2 * span_w[cm]).astype(np.int64),
+                                                                 np.maximum(span_w[cm] - 1, 0)))
+            cv = np.where(is_val[cm], lo + u2 * (hi - lo), 0.0)
             pe = torch.from_numpy(ce).to(self.dev)
             pb = torch.from_numpy(cb).to(self.dev)
             pimg = img[torch.from_numpy(pending).to(self.dev)].unsqueeze(1)
@@ -303,18 +329,28 @@ class ViTCampaign:
         """Trials k = block*G .. block*G + G - 1 of `layer`, one per image, folded into counters[layer]."""
         G = self.G
         ks = np.arange(block * G, (block + 1) * G, dtype=np.int64)
-        y = self._raw_output(layer)
-        elem, bit, mode_ix, value = self._sample(layer, ks, y)
-        ok = elem >= 0
+        main = torch.cuda.current_stream(self.dev)
         rows = self.model.rows_per_image(layer)
-        N = y.shape[1]
-        img = ks % G
-        grow = img * rows + np.where(ok, elem // N, 0)
-        gcol = np.where(ok, elem % N, 0)
-        inj = [K.Injection(row=int(r), col=int(c), bit=int(b)) if b >= 0 else
-               K.Injection(row=int(r), col=int(c), mode=L.GG_INJ_SET_VALUE, value=float(v))
-               for r, c, b, v, o in zip(grow, gcol, bit, value, ok) if o]
-        inj_dev = K.injections_to_device(inj, self.dev)
+        with torch.cuda.stream(self._side):
+            # every host <-> device copy of the sampling runs on the side stream: a pageable copy
+            # waits for its stream, and on the main one that is the previous block's forward
+            if self._y_layer != layer:  # the clean output of the layer, kept for its next blocks
+                self._y, self._y_layer = self._raw_output(layer), layer
+            y = self._y
+            elem, bit, mode_ix, value = self._sample(layer, ks, y)
+            ok = elem >= 0
+            N = y.shape[1]
+            img = ks % G
+            grow = img * rows + np.where(ok, elem // N, 0)
+            gcol = np.where(ok, elem % N, 0)
+            inj = [K.Injection(row=int(r), col=int(c), bit=int(b)) if b >= 0 else
+                   K.Injection(row=int(r), col=int(c), mode=L.GG_INJ_SET_VALUE, value=float(v))
+                   for r, c, b, v, o in zip(grow, gcol, bit, value, ok) if o]
+            inj_dev = K.injections_to_device(inj, self.dev)
+            okd = torch.from_numpy(ok).to(self.dev)
+        main.wait_stream(self._side)
+        for t in (y, inj_dev, okd):
+            t.record_stream(main)
         logits = self.model.resume(layer, self.cache, G, protect=True, injections={layer: inj_dev})
         lg = logits.float()
         pred = lg.argmax(dim=1)
@@ -322,7 +358,6 @@ class ViTCampaign:
         loss = torch.nn.functional.cross_entropy(lg, self.clean_pred, reduction="none")
         dl = torch.nan_to_num(loss - self.clean_loss, nan=LOSS_CLAMP, posinf=LOSS_CLAMP, neginf=-LOSS_CLAMP)
         dl_fx = torch.round(dl.clamp(-LOSS_CLAMP, LOSS_CLAMP).double() * LOSS_FX).to(torch.int64)
-        okd = torch.from_numpy(ok).to(self.dev)
         mism = (pred != self.clean_pred) & okd
         det = self._image_flags(layer) & okd
         if not self.model.layer(layer).protected:
