@@ -1416,6 +1416,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // Same association as fold_band (per column half over ascending tiles, then the halves).
       // The reducer's acquire-add and the barrier above order the loads.
       const bool every_row = ef == 1;
+#ifdef GG_TRACE
+      if (every_row && threadIdx.x == 0 && g_trace != nullptr)  // tiny tail: the fold starts
+        g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + 26] = clock64();
+#endif
       const int nb = every_row ? p.m_tiles : ef - 1;  // bands folded here
       const int nrows = nb * BM;
       const int tj = min(static_cast<int>(threadIdx.x) / BM, 1);
@@ -1498,6 +1502,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         if (every_row) {
           publish_summary<INT>(p, lane, bn, bk);
+#ifdef GG_TRACE
+          if (lane == 0 && g_trace != nullptr)  // tiny tail: the summary is out
+            g_trace[static_cast<size_t>(blockIdx.x) * TRACE_TILES * TRACE_EV + 27] = clock64();
+#endif
         } else {  // the band into the launch count; the band completing it publishes
           int last = 0;
           unsigned long long fin_rows = 0, fin_key = 0;

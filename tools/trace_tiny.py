@@ -62,7 +62,5 @@ for protect in (False, True):
         if r[24] > 0:
             line += (f" || LAST: before atomic {f(24)} acq_rel add {int(r[25] - r[24])} to closing barrier"
                      f" {int(r[26] - r[25])} all-thread fold + summary {int(r[27] - r[26])}")
-            r1 = t[c, 1]
-            line += (f" [loads+fold {int(r1[24] - r[26])} check+stores {int(r1[25] - r1[24])}"
-                     f" to barrier {int(r1[26] - r1[25])} summary {int(r[27] - r1[26])}]")
+
         print(line)
