@@ -335,6 +335,15 @@ GG_API int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int6
 GG_API int gg_add_layernorm(int32_t dtype, const void* h, const void* y, int64_t rows, int64_t D,
                             const float* gamma, const float* beta, float eps, void* h_out,
                             void* ln_out, const float* w_pred, uint64_t* pred_out, void* stream);
+/* The ViT embedding's tail in one pass: the residual stream h_out [B*T, D] is
+ * row (b, 0) = cls + pos[0] and row (b, t) = e[b*(T-1) + t-1] + pos[t] (t >= 1),
+ * each sum rounded to dtype like torch's add (e: the patch-embedding GEMM's
+ * output [B*(T-1), D], pos [T, D], cls [D]), then ln_out = LN(h_out) * gamma +
+ * beta as gg_add_layernorm (w_pred / pred_out likewise). */
+GG_API int gg_embed_layernorm(int32_t dtype, const void* e, const void* pos, const void* cls, int64_t B,
+                              int64_t T, int64_t D, const float* gamma, const float* beta, float eps,
+                              void* h_out, void* ln_out, const float* w_pred, uint64_t* pred_out,
+                              void* stream);
 /* If w_pred != NULL (the consumer layer's gg_checksum_aux vector, fp32 w_sum),
  * also pred_out[row] = sum_k ln_out[row,k] * w_pred[k] over the STORED (rounded)
  * ln_out values, as an fp32 (hi, lo) pair with lo = 0 (a per-lane fp32 FMA chain

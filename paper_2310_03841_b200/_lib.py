@@ -50,6 +50,7 @@ EXPORTED_SYMBOLS = (
     "gg_minmax",
     "gg_int_finish",
     "gg_add_layernorm",
+    "gg_embed_layernorm",
 )
 
 
@@ -183,6 +184,9 @@ def load(path: Path | None = None):
     lib.gg_add_layernorm.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, ctypes.c_float,
                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     lib.gg_add_layernorm.restype = c_int32
+    lib.gg_embed_layernorm.argtypes = [c_int32, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p,
+                                       c_void_p, ctypes.c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+    lib.gg_embed_layernorm.restype = c_int32
     lib.gg_round_f64_to.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p]
     _lib = lib
     return lib

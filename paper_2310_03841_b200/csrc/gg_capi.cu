@@ -116,6 +116,13 @@ int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int64_t ldy
   return gg::launch_int_finish(Y, B, T, N, ldy, relu, shift, qkv, H, static_cast<cudaStream_t>(stream));
 }
 
+int gg_embed_layernorm(int32_t dtype, const void* e, const void* pos, const void* cls, int64_t B, int64_t T,
+                       int64_t D, const float* gamma, const float* beta, float eps, void* h_out, void* ln_out,
+                       const float* w_pred, uint64_t* pred_out, void* stream) {
+  return gg::launch_embed_layernorm(dtype, e, pos, cls, B, T, D, gamma, beta, eps, h_out, ln_out, w_pred,
+                                    reinterpret_cast<unsigned long long*>(pred_out), static_cast<cudaStream_t>(stream));
+}
+
 int gg_add_layernorm(int32_t dtype, const void* h, const void* y, int64_t rows, int64_t D, const float* gamma,
                      const float* beta, float eps, void* h_out, void* ln_out, const float* w_pred, uint64_t* pred_out,
                      void* stream) {

@@ -69,6 +69,10 @@ int launch_add_layernorm(int dtype, const void* h, const void* y, int64_t rows, 
                          const float* beta, float eps, void* h_out, void* ln_out, const float* w_pred,
                          unsigned long long* pred_out, cudaStream_t s);
 
+int launch_embed_layernorm(int dtype, const void* e, const void* pos, const void* cls, int64_t B, int64_t T,
+                           int64_t D, const float* gamma, const float* beta, float eps, void* h_out, void* ln_out,
+                           const float* w_pred, unsigned long long* pred_out, cudaStream_t s);
+
 // implemented in gg_locate.cu
 size_t locate_workspace_bytes(int64_t M, int64_t K);
 int launch_locate_tiles(int x_dtype, const void* X, int64_t M, int64_t K, int64_t ldx, const void* W, int64_t N,

@@ -85,18 +85,29 @@ constexpr int ln_min_blocks(int floats) { return floats <= 24 ? 4 : floats <= 32
 // four 256-thread blocks per SM at D = 768: the predicted-sum variant otherwise took more than
 // 64 registers, three blocks, and ran 25% slower (two or four rows per warp sharing the affine
 // parameter loads measured slower still).
-template <typename T, int CH, bool PRED>
+// EMB (the ViT embedding, emb_T tokens per image): row (b, t) of the residual stream is
+// cls + pos[0] for t = 0 and e[b, t - 1] + pos[t] otherwise (h = e, y = pos, cls below), the
+// sum rounded to T like torch's add -- the patch embedding's position add, class token and
+// first layer norm in one pass.
+template <typename T, int CH, bool PRED, bool EMB = false>
 // h_out may alias h (in-place residual update): neither is __restrict__.
 __global__ void __launch_bounds__(256, ln_min_blocks(CH * Vec<T>::N)) add_layernorm_kernel(const T* h, const T* __restrict__ y, int64_t rows, int D,
                                                             const float* __restrict__ gamma,
                                                             const float* __restrict__ beta, float eps, T* h_out,
                                                             T* __restrict__ ln_out, const float* __restrict__ w_pred,
-                                                            unsigned long long* __restrict__ pred_out) {
+                                                            unsigned long long* __restrict__ pred_out,
+                                                            const T* __restrict__ cls = nullptr, int emb_T = 0) {
   constexpr int V = Vec<T>::N;
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
   const T* hr = h + row * D;
+  const T* yr = y + row * D;
+  if constexpr (EMB) {
+    const int64_t b = row / emb_T, t = row - b * emb_T;
+    hr = t == 0 ? cls : h + (b * (emb_T - 1) + t - 1) * D;
+    yr = y + t * D;
+  }
   float v[CH][V];
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
@@ -104,7 +115,7 @@ __global__ void __launch_bounds__(256, ln_min_blocks(CH * Vec<T>::N)) add_layern
     Vec<T>::load(hr + col, v[c]);
     if (y != nullptr) {
       float t[V];
-      Vec<T>::load(y + row * D + col, t);
+      Vec<T>::load(yr + col, t);
 #pragma unroll
       for (int i = 0; i < V; ++i) v[c][i] += t[i];
       uint4 packed;  // the stored (rounded) residual is what LN sees
@@ -203,7 +214,63 @@ int launch_add_ln_t(const void* h, const void* y, int64_t rows, int D, const flo
   return check_launch("add_layernorm");
 }
 
+template <typename T>
+int launch_embed_ln_t(const void* e, const void* pos, const void* cls, int64_t B, int T_, int D, const float* gamma,
+                      const float* beta, float eps, void* h_out, void* ln_out, const float* w_pred,
+                      unsigned long long* pred_out, cudaStream_t s) {
+  constexpr int V = Vec<T>::N;
+  if (D % (32 * V) != 0) return fail(GG_EUNSUPPORTED, "embed_layernorm: D must be a multiple of 32 x 16 bytes");
+  const int ch = D / (32 * V);
+  const int64_t rows = B * T_;
+  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+  const T* ep = static_cast<const T*>(e);
+  const T* pp = static_cast<const T*>(pos);
+  const T* cp = static_cast<const T*>(cls);
+  T* ho = static_cast<T*>(h_out);
+  T* lo = static_cast<T*>(ln_out);
+  switch (ch) {
+#define GG_EMB_CASE(n)                                                                                            \
+  case n:                                                                                                        \
+    if (w_pred != nullptr)                                                                                       \
+      add_layernorm_kernel<T, n, true, true><<<grid, 256, 0, s>>>(ep, pp, rows, D, gamma, beta, eps, ho, lo, w_pred, \
+                                                                  pred_out, cp, T_);                             \
+    else                                                                                                         \
+      add_layernorm_kernel<T, n, false, true><<<grid, 256, 0, s>>>(ep, pp, rows, D, gamma, beta, eps, ho, lo,      \
+                                                                   w_pred, pred_out, cp, T_);                    \
+    break;
+    GG_EMB_CASE(1) GG_EMB_CASE(2) GG_EMB_CASE(3) GG_EMB_CASE(4) GG_EMB_CASE(5) GG_EMB_CASE(6) GG_EMB_CASE(8)
+#undef GG_EMB_CASE
+    default:
+      return fail(GG_EUNSUPPORTED, "embed_layernorm: row width not built (32 x 16-byte chunks x {1..6, 8})");
+  }
+  return check_launch("embed_layernorm");
+}
+
 }  // namespace
+
+int launch_embed_layernorm(int dtype, const void* e, const void* pos, const void* cls, int64_t B, int64_t T_,
+                           int64_t D, const float* gamma, const float* beta, float eps, void* h_out, void* ln_out,
+                           const float* w_pred, unsigned long long* pred_out, cudaStream_t s) {
+  if ((w_pred == nullptr) != (pred_out == nullptr)) return fail(GG_EINVAL, "embed_layernorm: w_pred needs pred_out");
+  if (B < 1 || T_ < 2 || D < 1) return fail(GG_EINVAL, "embed_layernorm: needs B >= 1, T >= 2 tokens, D >= 1");
+  if (e == nullptr || pos == nullptr || cls == nullptr || gamma == nullptr || beta == nullptr || h_out == nullptr ||
+      ln_out == nullptr)
+    return fail(GG_EINVAL, "embed_layernorm: null argument");
+  if ((reinterpret_cast<uintptr_t>(e) | reinterpret_cast<uintptr_t>(pos) | reinterpret_cast<uintptr_t>(cls) |
+       reinterpret_cast<uintptr_t>(h_out) | reinterpret_cast<uintptr_t>(ln_out) | reinterpret_cast<uintptr_t>(gamma) |
+       reinterpret_cast<uintptr_t>(beta) | reinterpret_cast<uintptr_t>(w_pred)) &
+      15)
+    return fail(GG_EINVAL, "embed_layernorm: tensors must be 16-byte aligned");
+  switch (dtype) {
+    case GG_BF16: return launch_embed_ln_t<__nv_bfloat16>(e, pos, cls, B, static_cast<int>(T_), static_cast<int>(D),
+                                                          gamma, beta, eps, h_out, ln_out, w_pred, pred_out, s);
+    case GG_F16: return launch_embed_ln_t<__half>(e, pos, cls, B, static_cast<int>(T_), static_cast<int>(D), gamma,
+                                                  beta, eps, h_out, ln_out, w_pred, pred_out, s);
+    case GG_F32: return launch_embed_ln_t<float>(e, pos, cls, B, static_cast<int>(T_), static_cast<int>(D), gamma,
+                                                 beta, eps, h_out, ln_out, w_pred, pred_out, s);
+    default: return fail(GG_EUNSUPPORTED, "embed_layernorm: dtype must be GG_BF16, GG_F16 or GG_F32");
+  }
+}
 
 int launch_add_layernorm(int dtype, const void* h, const void* y, int64_t rows, int64_t D, const float* gamma,
                          const float* beta, float eps, void* h_out, void* ln_out, const float* w_pred,

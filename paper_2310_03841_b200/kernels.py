@@ -716,6 +716,26 @@ def reduce(a: torch.Tensor, axis: int) -> torch.Tensor:
     return out
 
 
+def embed_layernorm(e: torch.Tensor, pos: torch.Tensor, cls: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
+                    eps: float, h_out: torch.Tensor, ln_out: torch.Tensor, w_pred: torch.Tensor | None = None,
+                    pred_out: torch.Tensor | None = None) -> None:
+    """gg_embed_layernorm: h_out[b, 0] = cls + pos[0], h_out[b, t] = e[b, t - 1] + pos[t] (rounded like
+    torch's add), ln_out = LN(h_out) * gamma + beta (+ the consumer's predicted sums)."""
+    dev = _require_cuda(e, pos, cls, gamma, beta, h_out, ln_out)
+    T, D = pos.shape
+    rows = h_out.shape[0]
+    if rows % T or e.shape != (rows // T * (T - 1), D) or cls.shape != (D,) or ln_out.shape != (rows, D):
+        raise ValueError("embed_layernorm: e [B*(T-1), D], pos [T, D], cls [D], h_out / ln_out [B*T, D]")
+    for t in (e, pos, cls, h_out, ln_out):
+        if not t.is_contiguous() or t.dtype != e.dtype:
+            raise ValueError("embed_layernorm takes contiguous tensors of one dtype")
+    L.check(L.load().gg_embed_layernorm(TORCH_TO_GG[e.dtype], e.data_ptr(), pos.data_ptr(), cls.data_ptr(),
+                                        rows // T, T, D, gamma.data_ptr(), beta.data_ptr(), float(eps),
+                                        h_out.data_ptr(), ln_out.data_ptr(), _ptr(w_pred), _ptr(pred_out),
+                                        _stream(dev)),
+            "gg_embed_layernorm")
+
+
 def add_layernorm(h: torch.Tensor, y: torch.Tensor | None, gamma: torch.Tensor, beta: torch.Tensor, eps: float,
                   ln_out: torch.Tensor, h_out: torch.Tensor | None = None, w_pred: torch.Tensor | None = None,
                   pred_out: torch.Tensor | None = None) -> None:

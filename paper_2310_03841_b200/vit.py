@@ -373,10 +373,12 @@ class ProtectedViT(torch.nn.Module):
         if start == 0:
             save(0, None, bf.patches)
             self._lin(0, bf.patches, bf.e, bf, protect, inj)
-            hv = h.view(B, T, D)
-            torch.add(bf.e.view(B, T - 1, D), self.pos[1:], out=hv[:, 1:])
-            hv[:, 0] = self.cls + self.pos[0]
-            self._ln_into(1, protect, bf, h, None, *self._ln(0))
+            # position add, class token and the first layer norm in one pass (gg_embed_layernorm)
+            feeds = self._feeds_pred(1, protect)
+            K.embed_layernorm(bf.e, self.pos, self.cls, *self._ln(0), self.cfg.ln_eps, h_out=h, ln_out=bf.a,
+                              w_pred=self.linears[1].pred_vector if feeds else None,
+                              pred_out=bf.pred if feeds else None)
+            bf.pred_valid = feeds
         for b in range(c.depth):
             base = 1 + 4 * b
             if start <= base:
