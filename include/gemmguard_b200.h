@@ -335,6 +335,11 @@ GG_API int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int6
 GG_API int gg_add_layernorm(int32_t dtype, const void* h, const void* y, int64_t rows, int64_t D,
                             const float* gamma, const float* beta, float eps, void* h_out,
                             void* ln_out, const float* w_pred, uint64_t* pred_out, void* stream);
+/* ViT patch extraction: images [B, C, H, W] (NCHW) -> the patch-embedding GEMM's
+ * input [B * (H/P) * (W/P), C * P * P], row (b, gy, gx), column (c, py, px); 16-byte
+ * copies (P * element size a multiple of 16 bytes, 16-byte aligned tensors). */
+GG_API int gg_patchify(int32_t dtype, const void* images, int64_t B, int64_t C, int64_t H, int64_t W,
+                       int64_t P, void* out, void* stream);
 /* The ViT embedding's tail in one pass: the residual stream h_out [B*T, D] is
  * row (b, 0) = cls + pos[0] and row (b, t) = e[b*(T-1) + t-1] + pos[t] (t >= 1),
  * each sum rounded to dtype like torch's add (e: the patch-embedding GEMM's

@@ -51,6 +51,7 @@ EXPORTED_SYMBOLS = (
     "gg_int_finish",
     "gg_add_layernorm",
     "gg_embed_layernorm",
+    "gg_patchify",
 )
 
 
@@ -187,6 +188,8 @@ def load(path: Path | None = None):
     lib.gg_embed_layernorm.argtypes = [c_int32, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p,
                                        c_void_p, ctypes.c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     lib.gg_embed_layernorm.restype = c_int32
+    lib.gg_patchify.argtypes = [c_int32, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p]
+    lib.gg_patchify.restype = c_int32
     lib.gg_round_f64_to.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p]
     _lib = lib
     return lib

@@ -116,6 +116,11 @@ int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int64_t ldy
   return gg::launch_int_finish(Y, B, T, N, ldy, relu, shift, qkv, H, static_cast<cudaStream_t>(stream));
 }
 
+int gg_patchify(int32_t dtype, const void* images, int64_t B, int64_t C, int64_t H, int64_t W, int64_t P, void* out,
+                void* stream) {
+  return gg::launch_patchify(dtype, images, B, C, H, W, P, out, static_cast<cudaStream_t>(stream));
+}
+
 int gg_embed_layernorm(int32_t dtype, const void* e, const void* pos, const void* cls, int64_t B, int64_t T,
                        int64_t D, const float* gamma, const float* beta, float eps, void* h_out, void* ln_out,
                        const float* w_pred, uint64_t* pred_out, void* stream) {

@@ -69,6 +69,8 @@ int launch_add_layernorm(int dtype, const void* h, const void* y, int64_t rows, 
                          const float* beta, float eps, void* h_out, void* ln_out, const float* w_pred,
                          unsigned long long* pred_out, cudaStream_t s);
 
+int launch_patchify(int dtype, const void* images, int64_t B, int64_t C, int64_t H, int64_t W, int64_t P, void* out,
+                    cudaStream_t s);
 int launch_embed_layernorm(int dtype, const void* e, const void* pos, const void* cls, int64_t B, int64_t T,
                            int64_t D, const float* gamma, const float* beta, float eps, void* h_out, void* ln_out,
                            const float* w_pred, unsigned long long* pred_out, cudaStream_t s);

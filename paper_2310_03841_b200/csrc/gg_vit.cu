@@ -246,7 +246,42 @@ int launch_embed_ln_t(const void* e, const void* pos, const void* cls, int64_t B
   return check_launch("embed_layernorm");
 }
 
+// images [B, C, H, W] -> patches [B * (H/P) * (W/P), C * P * P], row (b, gy, gx), column (c, py, px):
+// one thread per 16-byte piece, consecutive threads along the patch row (whole 32 B sectors
+// read from each image row, fully coalesced writes)
+__global__ void patchify_kernel(const uint4* __restrict__ img, int64_t B, int C, int H, int W, int P, int vec_per_seg,
+                                uint4* __restrict__ out) {
+  const int Gy = H / P, Gx = W / P;
+  const int64_t seg_per_row = static_cast<int64_t>(C) * P;  // (c, py) segments of one patch
+  const int64_t total = B * Gy * Gx * seg_per_row * vec_per_seg;
+  const int64_t vec_w = static_cast<int64_t>(W) / (P / vec_per_seg);  // 16-byte pieces per image row
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = i % vec_per_seg;
+    const int64_t seg = (i / vec_per_seg) % seg_per_row;
+    const int64_t row = i / (vec_per_seg * seg_per_row);
+    const int64_t c = seg / P, py = seg % P;
+    const int64_t b = row / (Gy * Gx), g = row % (Gy * Gx), gy = g / Gx, gx = g % Gx;
+    const int64_t src = ((b * C + c) * H + gy * P + py) * vec_w + gx * vec_per_seg + v;
+    out[i] = __ldg(img + src);
+  }
+}
+
 }  // namespace
+
+int launch_patchify(int dtype, const void* images, int64_t B, int64_t C, int64_t H, int64_t W, int64_t P, void* out,
+                    cudaStream_t s) {
+  const int elem = dtype == GG_F32 ? 4 : (dtype == GG_BF16 || dtype == GG_F16) ? 2 : 0;
+  if (elem == 0) return fail(GG_EUNSUPPORTED, "patchify: dtype must be GG_BF16, GG_F16 or GG_F32");
+  if (B < 1 || C < 1 || P < 1 || H % P || W % P) return fail(GG_EINVAL, "patchify: H and W must be multiples of P");
+  if ((P * elem) % 16 || (reinterpret_cast<uintptr_t>(images) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    return fail(GG_EUNSUPPORTED, "patchify: P * element size must be a multiple of 16 bytes, tensors 16-byte aligned");
+  const int vec_per_seg = static_cast<int>(P * elem / 16);
+  patchify_kernel<<<148 * 16, 256, 0, s>>>(static_cast<const uint4*>(images), B, static_cast<int>(C),
+                                          static_cast<int>(H), static_cast<int>(W), static_cast<int>(P), vec_per_seg,
+                                          static_cast<uint4*>(out));
+  return check_launch("patchify");
+}
 
 int launch_embed_layernorm(int dtype, const void* e, const void* pos, const void* cls, int64_t B, int64_t T_,
                            int64_t D, const float* gamma, const float* beta, float eps, void* h_out, void* ln_out,

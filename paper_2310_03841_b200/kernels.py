@@ -716,6 +716,18 @@ def reduce(a: torch.Tensor, axis: int) -> torch.Tensor:
     return out
 
 
+def patchify(images: torch.Tensor, P: int, out: torch.Tensor) -> None:
+    """gg_patchify: images [B, C, H, W] -> out [B * (H/P) * (W/P), C * P * P] (row (b, gy, gx),
+    column (c, py, px)), the patch-embedding GEMM's input."""
+    dev = _require_cuda(images, out)
+    B, C, H, W = images.shape
+    if not images.is_contiguous() or not out.is_contiguous() or out.dtype != images.dtype or \
+            out.shape != (B * (H // P) * (W // P), C * P * P):
+        raise ValueError("patchify: contiguous images [B, C, H, W] and out [B * H/P * W/P, C * P * P] of one dtype")
+    L.check(L.load().gg_patchify(TORCH_TO_GG[images.dtype], images.data_ptr(), B, C, H, W, P, out.data_ptr(),
+                                 _stream(dev)), "gg_patchify")
+
+
 def embed_layernorm(e: torch.Tensor, pos: torch.Tensor, cls: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
                     eps: float, h_out: torch.Tensor, ln_out: torch.Tensor, w_pred: torch.Tensor | None = None,
                     pred_out: torch.Tensor | None = None) -> None:

@@ -342,7 +342,10 @@ class ProtectedViT(torch.nn.Module):
         bf = self.buffers(B)
         c = self.cfg
         P, G = c.patch, c.grid
-        bf.patches.view(B, G, G, 3, P, P).copy_(images.view(B, 3, G, P, G, P).permute(0, 2, 4, 1, 3, 5))
+        if images.is_contiguous() and images.dtype == bf.patches.dtype and (P * images.element_size()) % 16 == 0:
+            K.patchify(images, P, bf.patches)  # 16-byte copies (torch's permuted copy is element-wise)
+        else:
+            bf.patches.view(B, G, G, 3, P, P).copy_(images.view(B, 3, G, P, G, P).permute(0, 2, 4, 1, 3, 5))
         return self._run(bf, 0, protect, injections, cache)
 
     def resume(self, start: int, cache: dict, B: int, *, protect: bool | None = None,

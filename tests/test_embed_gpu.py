@@ -37,3 +37,17 @@ def test_embed_layernorm_matches_torch_adds_then_layernorm(dtype, B, T, D):
     K.add_layernorm(want, None, gamma, beta, 1e-6, ln_out=a2, w_pred=w, pred_out=pred2)
     assert torch.equal(a.view(torch.uint8), a2.view(torch.uint8))
     assert torch.equal(pred, pred2)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16, torch.float32])
+@pytest.mark.parametrize("B,H,P", [(2, 224, 16), (3, 64, 8), (1, 32, 32)])
+def test_patchify_matches_the_permuted_copy(dtype, B, H, P):
+    if (P * torch.tensor([], dtype=dtype).element_size()) % 16:
+        pytest.skip("16-byte pieces")
+    g = torch.Generator(device="cuda").manual_seed(B * H + P)
+    img = torch.randn(B, 3, H, H, device="cuda", generator=g).to(dtype)
+    G = H // P
+    out = torch.empty(B * G * G, 3 * P * P, dtype=dtype, device="cuda")
+    K.patchify(img, P, out)
+    want = img.view(B, 3, G, P, G, P).permute(0, 2, 4, 1, 3, 5).reshape(B * G * G, 3 * P * P)
+    assert torch.equal(out, want)
