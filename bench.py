@@ -388,8 +388,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict:
                      "model_flops_per_image": gemm_f + attn_f},
         "coverage": cov,
         "e2e": e2e,
-        "gpu_launches": (layer_launches + 2 * cfg.depth + 1) * args.steps,
-        "gpu_launches_note": "per step: 50 K1 (protected GEMM) + 25 gg_add_layernorm; torch SDPA / copies not counted",
+        "gpu_launches": (layer_launches + 2 * cfg.depth + 2) * args.steps,
+        "gpu_launches_note": "per step: 50 K1 (protected GEMM) + gg_patchify + gg_embed_layernorm + 24 "
+                             "gg_add_layernorm; torch SDPA not counted",
         "clocks": clk.summary(),
     }
 
