@@ -63,7 +63,8 @@ enum gg_inj_mode { GG_INJ_BITFLIP = 0, GG_INJ_SET_VALUE = 1 }; /* injector.py:49
  * guard.py:10-11 / model.py:367-368, the activation of that value is what is
  * stored (model.finish_layer_output's GELU, model.py:281-285, 318-319). */
 enum gg_epilogue_act { GG_ACT_NONE = 0, GG_ACT_GELU_TANH = 1 /* bf16 / fp16 outputs */,
-                       GG_ACT_RELU = 2 /* int8 requantised outputs (c_dtype GG_I8) */ };
+                       GG_ACT_RELU = 2 /* int8 requantised outputs (c_dtype GG_I8) */,
+                       GG_ACT_RESIDUAL = 3 /* bf16 / fp16: C = residual + y (desc.residual) */ };
 
 enum gg_error {
   GG_OK = 0,
@@ -160,6 +161,13 @@ typedef struct gg_gemm_desc {
    * The check runs on y (guard.py:170: the GEMM output, before the layer glue); C is [M, N]
    * int8 (ldc in bytes). */
   int32_t requant_shift;
+
+  /* epilogue_act = GG_ACT_RESIDUAL (16-bit outputs): the stored output is the residual
+   * stream's update round(residual + y) of the checked GEMM output y (the check covers y,
+   * guard.py:170; the add is a transformer block's glue).  residual [M, N] (ld_res, the
+   * output type) must not alias C, so a replay can recompute the same bytes. */
+  const void* residual;
+  int64_t ld_res;
 } gg_gemm_desc;
 
 enum gg_b_layout { GG_B_NK = 0, GG_B_KN = 1 };

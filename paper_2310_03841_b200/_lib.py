@@ -24,7 +24,7 @@ GG_PER_SAMPLE, GG_BATCH_MEAN = 0, 1
 GG_INJ_OUTPUT, GG_INJ_ACCUMULATOR = 0, 1
 GG_B_NK, GG_B_KN = 0, 1
 GG_INJ_BITFLIP, GG_INJ_SET_VALUE = 0, 1
-GG_ACT_NONE, GG_ACT_GELU_TANH, GG_ACT_RELU = 0, 1, 2
+GG_ACT_NONE, GG_ACT_GELU_TANH, GG_ACT_RELU, GG_ACT_RESIDUAL = 0, 1, 2, 3
 GG_OK, GG_EINVAL, GG_ECUDA, GG_EWORKSPACE, GG_EUNSUPPORTED = 0, -1, -2, -3, -4
 
 # every symbol include/gemmguard_b200.h declares
@@ -107,6 +107,8 @@ class GGGemmDesc(ctypes.Structure):
         ("b_scratch", c_void_p),
         ("b_scratch_bytes", c_size_t),
         ("requant_shift", c_int32),
+        ("residual", c_void_p),
+        ("ld_res", c_int64),
     ]
 
 

@@ -89,7 +89,7 @@ constexpr int NSLOT = 4;                      // depth of the observed / predict
 // CTAs tens of microseconds behind on long-N shapes).
 constexpr int FQ = 16;
 constexpr int QAREA = (16 + 4 * FQ + 15) / 16 * 16;  // tmem slot + queued band ids
-constexpr int NBAR = 4 * STAGES + 4 + 4 * NSLOT + 2 * FQ;
+constexpr int NBAR = 4 * STAGES + 4 + 4 * NSLOT + 2 * FQ + 2 * EPI_WARPS;  // + the residual boxes' loads
 constexpr int W_SMEM = 16384;                 // checksum w-vector kept in shared memory when it fits
 constexpr int SMEM_BYTES = BAR_OFF + NBAR * 8 + QAREA /*tmem slot, finisher queue*/ + 3 * NSLOT * BM * 8 /*partial rings*/ +
                            2 * BN * 4 /*bias tiles*/ + W_SMEM + 1024 /*align*/;
@@ -393,7 +393,7 @@ __device__ __forceinline__ void stage_row(uint32_t box, int lane, const uint32_t
 // Epilogue activations applied to the stored encoding AFTER the observed row sum
 // (the check runs on the raw, rounded GEMM output: guard.py:10-11, model.py:367-368,
 // SURVEY §8(a) a4 (ii)); the activated value is rounded to the output type again.
-enum : int { ACT_NONE = 0, ACT_GELU_TANH = 1, ACT_RELU = 2 };
+enum : int { ACT_NONE = 0, ACT_GELU_TANH = 1, ACT_RELU = 2, ACT_RESIDUAL = 3 };
 
 // model.finish_layer_output's requantisation of an int32 output (model.py:312-316):
 // clip(((relu ? max(y, 0) : y) + 2^(s-1)) >> s, -128, 127), int32 wrap-around as NumPy
@@ -442,7 +442,8 @@ __device__ __forceinline__ float2 gelu_tanh_f32x2(float2 x) {
 template <int KIND, int OUT, bool PROTECT, bool CLAIM, int ACT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gg_protected_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                                  const __grid_constant__ CUtensorMap tmC, const Params p) {
+                                  const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
+                                  const Params p) {
   using T = KindTraits<KIND>;
   constexpr bool INT = (KIND == K_I8);
   constexpr int BK = BK_BYTES / T::ELEM;
@@ -480,7 +481,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* pempty_bar = pfull_bar + NSLOT;     // [NSLOT]
   uint64_t* fq_full = pempty_bar + NSLOT;       // [FQ] a split band id queued by the reducer
   uint64_t* fq_empty = fq_full + FQ;            // [FQ] taken by the finisher warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fq_empty + FQ);
+  uint64_t* rfull_bar = fq_empty + FQ;          // [2 * EPI_WARPS] a residual box landed (TMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull_bar + 2 * EPI_WARPS);
   int* end_fold = reinterpret_cast<int*>(tmem_slot + 1);  // the kernel-end fold: [0] 0 none, 1 every row,
                                                           // 1 + k: the k bands [1], [2]
   int* fq_band = reinterpret_cast<int*>(tmem_slot + 4);           // [FQ]
@@ -605,6 +607,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       mbar_init(&fq_full[b], 1);
       mbar_init(&fq_empty[b], 1);
     }
+    for (int b = 0; b < 2 * EPI_WARPS; ++b) {
+      mbar_init(&rfull_bar[b], 1);
+    }
     end_fold[0] = 0;
     fence_barrier_init();
     fence_proxy_async_smem();
@@ -646,6 +651,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int m = t / n_tiles, n = t - m * n_tiles;
         if (!pair_active(m)) continue;
         const int arow = m * 2 * BM + static_cast<int>(rank) * BM;
+
         const int brow = n * BN + static_cast<int>(rank) * (BN / 2);
         int rem = 0;  // kb % n_tiles
 #ifdef GG_TRACE
@@ -936,6 +942,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       return c < p.N ? __ldcg(bias_g + c) : 0u;
     };
     uint32_t bias_next = bias_of(0);
+    // the residual (ACT_RESIDUAL): this thread's row segment of 32 outputs, 16-byte loads
+    auto res_load = [&](bool ok, int rrow, int rcol0, uint32_t* dst) {
+      if constexpr (ACT == ACT_RESIDUAL && OUT16) {
+        const uint16_t* rr = static_cast<const uint16_t*>(p.residual) + static_cast<long long>(rrow) * p.ld_res + rcol0;
+        if (ok && rcol0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(rr) & 15) == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(rr) + q);
+            dst[4 * q] = u.x; dst[4 * q + 1] = u.y; dst[4 * q + 2] = u.z; dst[4 * q + 3] = u.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t lo = ok && rcol0 + 2 * i < p.N ? rr[2 * i] : 0u;
+            const uint32_t hi = ok && rcol0 + 2 * i + 1 < p.N ? rr[2 * i + 1] : 0u;
+            dst[i] = lo | (hi << 16);
+          }
+        }
+      }
+    };
+    // the residual through TMA: each epilogue warp's 32 x 32 box loaded into its staging box (the
+    // output is then written over it and stored), the next chunk's requested after a store
+    const bool r_tma = ACT == ACT_RESIDUAL && OUT16 && p.r_tma != 0 && c_tma;
+    uint32_t rph = 0;      // phase bits of this warp's two residual boxes
+    bool res_ahead = false;  // the tile's first chunk was requested at the previous tile's last
+    auto res_issue = [&](int box_i, int rcol0, int rrow0) {
+      uint64_t* bar = &rfull_bar[2 * (warp - W_EPI0) + box_i];
+      mbar_arrive_expect_tx(bar, 32 * CBOX * 2);
+      tma_load_2d_cta(smC + (warp - W_EPI0) * CST_BYTES + box_i * 2048, &tmR, bar, rcol0, rrow0);
+    };
+    uint32_t rw_next[ACT == ACT_RESIDUAL ? 16 : 1];
+    if constexpr (ACT == ACT_RESIDUAL && OUT16) {
+      if (!p.replay && !r_tma && n_seq > 0) {
+        const int t2 = tile_at(0);
+        const int m2 = t2 / n_tiles, n2 = t2 - m2 * n_tiles;
+        const int row2 = m2 * 2 * BM + static_cast<int>(rank) * BM + (warp & 3) * 32 + lane;
+        res_load(row2 < p.M, row2, n2 * BN + 32 * (4 * ((warp - W_EPI0) >> 2)), rw_next);
+      }
+    }
     for (int i_seq = 0; i_seq < n_seq; ++i_seq) {
         const int t = tile_at(i_seq);
       const int m = t / n_tiles, n = t - m * n_tiles;
@@ -996,6 +1041,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll 1
       for (int c = c_begin; c < c_end; ++c) {
         const int col0 = n0 + 32 * c;
+        // the residual's 32 values of this row and chunk were requested one chunk ahead (their
+        // latency overlaps a whole chunk); request the next chunk's -- the next tile's first one
+        // after the last (replay walks sparse tiles: loaded here instead)
+        uint32_t rw[ACT == ACT_RESIDUAL ? 16 : 1];
+        if constexpr (ACT == ACT_RESIDUAL && OUT16) {
+          if (r_tma) {
+            if (c == c_begin && !res_ahead && lane == 0) {  // a tile's first chunk, not requested ahead
+              bulk_wait_read<1>();                          // the box's store two chunks ago has read it
+              res_issue(cbuf, col0, row0 + 32 * eg);
+            }
+            if (c == c_begin) res_ahead = false;
+          } else if (p.replay) {
+            res_load(row_ok, row, col0, rw);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) rw[i] = rw_next[i];
+            if (c + 1 < c_end) {
+              res_load(row_ok, row, col0 + 32, rw_next);
+            } else if (i_seq + 1 < n_seq) {
+              const int t2 = tile_at(i_seq + 1);
+              const int m2 = t2 / n_tiles, n2 = t2 - m2 * n_tiles;
+              const int row2 = m2 * 2 * BM + static_cast<int>(rank) * BM + tid;
+              res_load(row2 < p.M, row2, n2 * BN + 32 * c_begin, rw_next);
+            }
+          }
+        }
         uint32_t r[32];
         tmem_ld_32x32b_x32(
             tmem_base + (static_cast<uint32_t>(eg * 32) << 16) + static_cast<uint32_t>(buf * BN + 32 * c), r);
@@ -1138,6 +1209,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             o[i] = (OUT == O_BF16) ? pack_bf16x2(g.x, g.y) : pack_f16x2(g.x, g.y);
           }
         }
+        if constexpr (ACT == ACT_RESIDUAL && OUT16) {
+          // the residual stream's update fused: stored = round(residual + y) of the checked y (the
+          // bytes a separate add would produce); the residual is read-only here (replayable)
+          if (r_tma) {
+            mbar_wait(&rfull_bar[2 * (warp - W_EPI0) + cbuf], (rph >> cbuf) & 1u);
+            rph ^= 1u << cbuf;
+            const uint32_t rrow = smem_u32(smC + (warp - W_EPI0) * CST_BYTES + cbuf * 2048) +
+                                  static_cast<uint32_t>(lane * 64);  // SWIZZLE_64B, as stage_row
+            const int sw = (lane >> 1) & 3;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 u = lds128(rrow + static_cast<uint32_t>((q ^ sw) << 4));
+              rw[4 * q] = u.x; rw[4 * q + 1] = u.y; rw[4 * q + 2] = u.z; rw[4 * q + 3] = u.w;
+            }
+          }
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float2 yv = (OUT == O_BF16) ? bf16x2_to_f32x2(o[i])
+                                                : __half22float2(*reinterpret_cast<const __half2*>(&o[i]));
+              const float2 hv = (OUT == O_BF16) ? bf16x2_to_f32x2(rw[i])
+                                                : __half22float2(*reinterpret_cast<const __half2*>(&rw[i]));
+              const float2 sv = add_f32x2(hv, yv);
+              o[i] = (OUT == O_BF16) ? pack_bf16x2(sv.x, sv.y) : pack_f16x2(sv.x, sv.y);
+            }
+          }
+        }
         if constexpr (OUT == O_I8) {  // the checked int32 outputs requantised, four per word in o[0..7]
           uint32_t h8[8];
 #pragma unroll
@@ -1149,7 +1247,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (c_tma) {
           // coalesced store: this warp's 32 rows x 32 columns through a swizzled smem box + TMA
           uint8_t* boxp = smC + e * CST_BYTES + (BOX2 ? cbuf * 2048 : 0);
-          if (lane == 0) {
+          if (lane == 0 && !r_tma) {  // (with r_tma the box holds this chunk's residual: already ours)
             if constexpr (BOX2) bulk_wait_read<1>();  // the box written two chunks ago has been read
             else bulk_wait_read<0>();
           }
@@ -1160,6 +1258,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (lane == 0) {
             tma_store_2d(&tmC, boxp, col0, row0 + 32 * eg);
             bulk_commit();
+          }
+          if (r_tma) {  // the next chunk's residual into the other box, once the store two chunks ago
+                        // has read it -- at a tile's last chunk, the next tile's first (when it has one)
+            int ncol = -1, nrow = 0;
+            if (c + 1 < c_end) {
+              ncol = col0 + 32;
+              nrow = row0 + 32 * eg;
+            } else if (i_seq + 1 < n_seq) {
+              const int t2 = tile_at(i_seq + 1);
+              const int m2 = t2 / n_tiles, n2 = t2 - m2 * n_tiles;
+              if (c_begin < min(BN / 32, (p.N - n2 * BN + 31) / 32)) {
+                ncol = n2 * BN + 32 * c_begin;
+                nrow = m2 * 2 * BM + static_cast<int>(rank) * BM + 32 * eg;
+                res_ahead = true;
+              }
+            }
+            if (ncol >= 0 && lane == 0) {
+              bulk_wait_read<1>();
+              res_issue(cbuf ^ 1, ncol, nrow);
+            }
           }
           if constexpr (BOX2) cbuf ^= 1;
           GG_LAP(tr_st);

@@ -230,8 +230,8 @@ int max_coresident_pairs(int dev) {
 }
 
 template <int KIND, int OUT, bool PROTECT, bool CLAIM = false, int ACT = pair::ACT_NONE>
-int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p, int grid,
-                         cudaStream_t s) {
+int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tr,
+                         const Params& p, int grid, cudaStream_t s) {
   auto kern = pair::gg_protected_gemm_pair_kernel<KIND, OUT, PROTECT, CLAIM, ACT>;
   int dev;
   int rc = current_device(dev);
@@ -239,7 +239,7 @@ int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
   rc = configure_instance<KIND, OUT, PROTECT, CLAIM, ACT>(dev);
   if (rc) return rc;
 #ifdef GG_NO_PDL
-  kern<<<grid, pair::THREADS, pair::SMEM_BYTES, s>>>(ta, tb, tc, p);
+  kern<<<grid, pair::THREADS, pair::SMEM_BYTES, s>>>(ta, tb, tc, tr, p);
 #else
   // programmatic dependent launch: the CTA setup overlaps the previous kernel's tail (the
   // kernel waits on griddepcontrol before touching memory)
@@ -253,31 +253,35 @@ int launch_pair_instance(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p);
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tr, p);
 #endif
   return check_launch("protected_gemm_pair");
 }
 
 template <int KIND, int OUT>
 int dispatch_protect(bool protect, int act, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                     const Params& p, int grid, cudaStream_t s) {
+                     const CUtensorMap& tr, const Params& p, int grid, cudaStream_t s) {
   if constexpr ((KIND == K_BF16 && OUT == O_BF16) || (KIND == K_F16 && OUT == O_F16)) {
     if (act == GG_ACT_GELU_TANH)
-      return protect ? launch_pair_instance<KIND, OUT, true, false, pair::ACT_GELU_TANH>(ta, tb, tc, p, grid, s)
-                     : launch_pair_instance<KIND, OUT, false, false, pair::ACT_GELU_TANH>(ta, tb, tc, p, grid, s);
+      return protect ? launch_pair_instance<KIND, OUT, true, false, pair::ACT_GELU_TANH>(ta, tb, tc, tr, p, grid, s)
+                     : launch_pair_instance<KIND, OUT, false, false, pair::ACT_GELU_TANH>(ta, tb, tc, tr, p, grid, s);
+    if (act == GG_ACT_RESIDUAL)
+      return protect ? launch_pair_instance<KIND, OUT, true, false, pair::ACT_RESIDUAL>(ta, tb, tc, tr, p, grid, s)
+                     : launch_pair_instance<KIND, OUT, false, false, pair::ACT_RESIDUAL>(ta, tb, tc, tr, p, grid, s);
   }
   if constexpr (OUT == O_I8) {
     if (act == GG_ACT_RELU)
-      return protect ? launch_pair_instance<KIND, OUT, true, false, pair::ACT_RELU>(ta, tb, tc, p, grid, s)
-                     : launch_pair_instance<KIND, OUT, false, false, pair::ACT_RELU>(ta, tb, tc, p, grid, s);
+      return protect ? launch_pair_instance<KIND, OUT, true, false, pair::ACT_RELU>(ta, tb, tc, tr, p, grid, s)
+                     : launch_pair_instance<KIND, OUT, false, false, pair::ACT_RELU>(ta, tb, tc, tr, p, grid, s);
   }
   if (act != GG_ACT_NONE)
-    return fail(GG_EUNSUPPORTED, "protected_gemm: GELU needs bf16 / fp16 outputs, ReLU requantised int8 outputs");
-  if (!protect) return launch_pair_instance<KIND, OUT, false>(ta, tb, tc, p, grid, s);
+    return fail(GG_EUNSUPPORTED,
+                "protected_gemm: GELU / residual need bf16 / fp16 outputs, ReLU requantised int8 outputs");
+  if (!protect) return launch_pair_instance<KIND, OUT, false>(ta, tb, tc, tr, p, grid, s);
   if constexpr (KIND == K_TF32) {  // claimed split-band folds (see the kernel)
-    if (!p.few_tiles && !p.tiny && p.n_tiles >= 8) return launch_pair_instance<KIND, OUT, true, true>(ta, tb, tc, p, grid, s);
+    if (!p.few_tiles && !p.tiny && p.n_tiles >= 8) return launch_pair_instance<KIND, OUT, true, true>(ta, tb, tc, tr, p, grid, s);
   }
-  return launch_pair_instance<KIND, OUT, true>(ta, tb, tc, p, grid, s);
+  return launch_pair_instance<KIND, OUT, true>(ta, tb, tc, tr, p, grid, s);
 }
 
 }  // namespace
@@ -420,6 +424,13 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   std::memset(&tc, 0, sizeof(tc));
   int c_tma = ((reinterpret_cast<uintptr_t>(d->C) & 15) == 0 && (d->ldc * out_elem) % 16 == 0) ? 1 : 0;
   if (c_tma && make_output_map(&tc, cdt, out_elem, d->C, d->N, d->M, d->ldc * out_elem) != 0) c_tma = 0;
+  // the fused residual update's input, through the same 32 x 32 boxes as the stores
+  CUtensorMap tr = tc;
+  int r_tma = 0;
+  if (d->epilogue_act == GG_ACT_RESIDUAL && c_tma && d->residual != nullptr &&
+      (reinterpret_cast<uintptr_t>(d->residual) & 15) == 0 && (d->ld_res * out_elem) % 16 == 0 &&
+      make_output_map(&tr, cdt, out_elem, const_cast<void*>(d->residual), d->N, d->M, d->ld_res * out_elem) == 0)
+    r_tma = 1;
 
   Params p{};
   p.M = static_cast<int>(d->M);
@@ -435,6 +446,14 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
   p.ldc = d->ldc;
   p.c_tma = c_tma;
   p.requant_shift = d->requant_shift;
+  if (d->epilogue_act == GG_ACT_RESIDUAL) {
+    if (d->residual == nullptr || d->ld_res < d->N)
+      return fail(GG_EINVAL, "protected_gemm: GG_ACT_RESIDUAL needs the residual [M, N] (ld_res >= N)");
+    if (d->residual == d->C) return fail(GG_EINVAL, "protected_gemm: the residual must not alias C (replay reads it)");
+  }
+  p.residual = d->residual;
+  p.ld_res = d->ld_res;
+  p.r_tma = r_tma;
 #ifdef GG_DIAGNOSTICS
   if (std::getenv("GG_NO_CTMA")) p.c_tma = 0;  // diagnostics: direct vector stores from registers
 #endif
@@ -519,19 +538,19 @@ int launch_protected_gemm(const gg_gemm_desc* d, bool replay, cudaStream_t s) {
 
   switch (kind) {
     case K_BF16:
-      rc = out == O_BF16 ? dispatch_protect<K_BF16, O_BF16>(protect, d->epilogue_act, ta, tb, tc, p, grid, s)
-                         : dispatch_protect<K_BF16, O_F32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
+      rc = out == O_BF16 ? dispatch_protect<K_BF16, O_BF16>(protect, d->epilogue_act, ta, tb, tc, tr, p, grid, s)
+                         : dispatch_protect<K_BF16, O_F32>(protect, d->epilogue_act, ta, tb, tc, tr, p, grid, s);
       break;
     case K_F16:
-      rc = out == O_F16 ? dispatch_protect<K_F16, O_F16>(protect, d->epilogue_act, ta, tb, tc, p, grid, s)
-                        : dispatch_protect<K_F16, O_F32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
+      rc = out == O_F16 ? dispatch_protect<K_F16, O_F16>(protect, d->epilogue_act, ta, tb, tc, tr, p, grid, s)
+                        : dispatch_protect<K_F16, O_F32>(protect, d->epilogue_act, ta, tb, tc, tr, p, grid, s);
       break;
     case K_TF32:
-      rc = dispatch_protect<K_TF32, O_F32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
+      rc = dispatch_protect<K_TF32, O_F32>(protect, d->epilogue_act, ta, tb, tc, tr, p, grid, s);
       break;
     default:
-      rc = out == O_I32 ? dispatch_protect<K_I8, O_I32>(protect, d->epilogue_act, ta, tb, tc, p, grid, s)
-                        : dispatch_protect<K_I8, O_I8>(protect, d->epilogue_act, ta, tb, tc, p, grid, s);
+      rc = out == O_I32 ? dispatch_protect<K_I8, O_I32>(protect, d->epilogue_act, ta, tb, tc, tr, p, grid, s)
+                        : dispatch_protect<K_I8, O_I8>(protect, d->epilogue_act, ta, tb, tc, tr, p, grid, s);
   }
   if (rc == 0 && batch_mean)
     rc = launch_batch_mean_finish(d->M, d->mu, d->lo, d->hi, static_cast<const double*>(d->d), d->flags, d->max_disc,

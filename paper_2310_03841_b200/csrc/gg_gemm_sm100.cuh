@@ -74,6 +74,9 @@ struct Params {
                         // 1024 / 2048 force the contiguous / strided schedule
   const void* pred_in;  // [M] predicted row sums (fp32 (hi, lo) pairs) supplied by X's producer, or null
   int requant_shift;    // O_I8: the stored output's requantisation shift
+  const void* residual; // ACT_RESIDUAL: [M, N] of the output type, stored = residual + y
+  long long ld_res;
+  int r_tma;            // 1: the residual is read through TMA boxes (tmR) into the staging boxes
   int replay;           // 1: only active bands, compare against old C
   int* changed;
   Workspace ws;

@@ -156,6 +156,7 @@ def build_desc(
     act: int = L.GG_ACT_NONE,
     pred_in: torch.Tensor | None = None,
     requant_shift: int = 0,
+    residual: torch.Tensor | None = None,
 ) -> L.GGGemmDesc:
     M, K = x.shape
     N = w.shape[0]
@@ -193,6 +194,12 @@ def build_desc(
     d.epilogue_act = int(act)
     d.pred_in = _ptr(pred_in) if protect else None
     d.requant_shift = int(requant_shift)
+    if residual is not None:
+        if residual.shape != y.shape or residual.dtype != y.dtype or residual.stride(1) != 1:
+            raise ValueError("residual must be [M, N] of the output dtype with contiguous rows")
+        if residual.data_ptr() == y.data_ptr():
+            raise ValueError("residual must not alias the output (a replay re-reads it)")
+        d.residual, d.ld_res = residual.data_ptr(), residual.stride(0)
     return d
 
 
@@ -319,6 +326,7 @@ def protected_gemm(
     act: int = L.GG_ACT_NONE,
     pred_in: torch.Tensor | None = None,
     requant_shift: int = 0,
+    residual: torch.Tensor | None = None,
 ) -> tuple[torch.Tensor, CheckResult | None]:
     """K1: y = x @ w.T + bias with the fused checksum check (one launch).
 
@@ -331,6 +339,8 @@ def protected_gemm(
     int8 operands with out_dtype=torch.int8 and requant_shift s store the requantised hidden
     state clip(((relu ? max(y, 0) : y) + 2^(s-1)) >> s, -128, 127) of the checked int32 y
     (act=GG_ACT_RELU for the relu; model.finish_layer_output's elementwise part).
+    residual [M, N] (16-bit outputs): the stored output is round(residual + y) of the checked y
+    (a transformer block's residual update fused; act becomes GG_ACT_RESIDUAL).
     Returns (y, CheckResult or None when protect=False).
     """
     dev = _require_cuda(x, w, bias)
@@ -354,7 +364,9 @@ def protected_gemm(
         inj_dev, n_inj = None, 0
     desc = build_desc(x, w, y, bias, protect=protect, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo,
                       hi=hi, statistic=statistic, result=result, inj_dev=inj_dev, n_inj=n_inj, ws=ws, act=act,
-                      pred_in=_check_pred(pred_in, M), requant_shift=requant_shift)
+                      pred_in=_check_pred(pred_in, M), requant_shift=requant_shift, residual=residual)
+    if residual is not None:
+        desc.epilogue_act = L.GG_ACT_RESIDUAL
     L.check(L.load().gg_protected_gemm(ctypes.byref(desc), _stream(dev)), "gg_protected_gemm")
     return y, (result if protect else None)
 
@@ -483,6 +495,7 @@ def replay_tiles(
     act: int = L.GG_ACT_NONE,
     pred_in: torch.Tensor | None = None,
     requant_shift: int = 0,
+    residual: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """K4: recompute only the M-bands holding a flagged row, in place in y.
 
@@ -498,7 +511,9 @@ def replay_tiles(
     ws = workspace(M, N, dev, ws_key)
     desc = build_desc(x, w, y, bias, protect=True, w_sum=w_sum, w_aux=w_aux, bias_sum=bias_sum, mu=mu, lo=lo, hi=hi,
                       statistic=statistic, result=result, ws=ws, replay_rows=replay_rows, changed=changed, act=act,
-                      pred_in=_check_pred(pred_in, M), requant_shift=requant_shift)
+                      pred_in=_check_pred(pred_in, M), requant_shift=requant_shift, residual=residual)
+    if residual is not None:
+        desc.epilogue_act = L.GG_ACT_RESIDUAL
     L.check(L.load().gg_replay_tiles(ctypes.byref(desc), _stream(dev)), "gg_replay_tiles")
     return changed
 

@@ -152,13 +152,18 @@ class ProtectedLinear(torch.nn.Module):
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, result: K.CheckResult | None = None,
                 injections: torch.Tensor | None = None, protect: bool | None = None,
-                pred_in: torch.Tensor | None = None) -> torch.Tensor:
-        """pred_in: x . w_sum computed by x's producer (kernels.add_layernorm with w_pred=self.aux)."""
+                pred_in: torch.Tensor | None = None, residual: torch.Tensor | None = None) -> torch.Tensor:
+        """pred_in: x . w_sum computed by x's producer (kernels.add_layernorm with w_pred=self.aux).
+        residual: the stored output is residual + y (the check covers y; no fused activation)."""
         p = self.protected if protect is None else protect
+        kw = self._kw(p)
+        if residual is not None:
+            kw.pop("act")
         y, res = K.protected_gemm(x, self.weight, self.bias, out=out, result=result, injections=injections,
-                                  pred_in=pred_in if p else None, **self._kw(p))
+                                  pred_in=pred_in if p else None, residual=residual, **kw)
         self.result = res
         self.last_pred_in = pred_in if p else None
+        self.last_residual = residual
         return y
 
     @property
@@ -177,7 +182,11 @@ class ProtectedLinear(torch.nn.Module):
         layers with a fused activation replay whole bands (their check needs the raw output)."""
         kw = self._kw(True)
         kw.pop("protect")
-        if granularity == "tile" and self.act == L.GG_ACT_NONE:
+        residual = getattr(self, "last_residual", None)
+        if residual is not None:
+            kw.pop("act")
+            kw["residual"] = residual
+        if granularity == "tile" and self.act == L.GG_ACT_NONE and residual is None:
             ch, _ = K.replay_located(x, self.weight, self.bias, y, result, w_sum=self.w_sum,
                                      bias_sum=self.bias_sum, mu=kw["mu"], lo=kw["lo"], hi=kw["hi"],
                                      f32_mode=self.f32_mode, w_split=self.w_split, ws_key=kw["ws_key"],
@@ -194,8 +203,8 @@ class ProtectedLinear(torch.nn.Module):
 
 def _located(lin: "ProtectedLinear", x: torch.Tensor, y: torch.Tensor, res: K.CheckResult) -> list:
     """The (128-row band, 256-column tile) pairs column checksums place the flagged faults in."""
-    if lin.act != L.GG_ACT_NONE:
-        return []
+    if lin.act != L.GG_ACT_NONE or getattr(lin, "last_residual", None) is not None:
+        return []  # (the stored output is not the GEMM's alone)
     mask, _ = K.locate_tiles(x, lin.weight, lin.bias, y, res, mu=lin.mu)
     return [tuple(t) for t in mask.nonzero().tolist()]
 
@@ -216,6 +225,7 @@ class _Buffers:
     pred: torch.Tensor | None = None  # [B*T] predicted sums of the next GEMM, from the layer norm
     results: dict = field(default_factory=dict)
     o_view: torch.Tensor | None = None  # the proj input: the attention output itself when contiguous, else o
+    h2: torch.Tensor | None = None  # the residual stream after proj when the GEMMs add it (fused_residual)
 
 
 class ProtectedViT(torch.nn.Module):
@@ -231,6 +241,9 @@ class ProtectedViT(torch.nn.Module):
         D = cfg.dim
         fused_gelu = dtype in (torch.bfloat16, torch.float16)
         self.fused_gelu = fused_gelu
+        # proj and fc2 store the residual stream's update h + y themselves (GG_ACT_RESIDUAL: the
+        # check still covers y), so the layer norms after them read one matrix instead of two
+        self.fused_residual = fused_gelu
         mk = lambda i, n, k_in, k_out, act=L.GG_ACT_NONE, s=1.0: ProtectedLinear(  # noqa: E731
             i, n, k_in, k_out, dtype=dtype, device=dev, generator=g, act=act, f32_mode=f32_mode, init_scale=s)
         layers = [mk(0, "patch_embed", cfg.patch_dim, D)]
@@ -275,7 +288,8 @@ class ProtectedViT(torch.nn.Module):
                           a=e(B * T, D), qkv=e(B * T, 3 * D), o=e(B * T, D), y=e(B * T, D), f=e(B * T, c.mlp),
                           cls_in=e(B, D), logits=torch.empty(B, c.classes, device=dev,
                                                              dtype=torch.int32 if dt == torch.int8 else dt),
-                          pred=torch.empty(B * T, device=dev, dtype=torch.int64))
+                          pred=torch.empty(B * T, device=dev, dtype=torch.int64),
+                          h2=e(B * T, D) if self.fused_residual else None)
             for lin in self.linears:
                 M = B * self.rows_per_image(lin.index)
                 bf.results[lin.index] = K.CheckResult.empty(M, lin.integer, dev)
@@ -302,13 +316,13 @@ class ProtectedViT(torch.nn.Module):
         bf.pred_valid = feeds
 
     def _lin(self, i: int, x: torch.Tensor, out: torch.Tensor, bf: _Buffers, protect: bool | None,
-             injections: dict | None, pred: bool = False) -> torch.Tensor:
+             injections: dict | None, pred: bool = False, residual: torch.Tensor | None = None) -> torch.Tensor:
         lin = self.linears[i]
         inj = injections.get(i) if injections else None
         use_pred = pred and getattr(bf, "pred_valid", False) and self._feeds_pred(i, protect)
         y = lin(x, out=out, result=bf.results[i], injections=inj,
                 protect=None if protect is None else (protect and lin.protected),
-                pred_in=bf.pred if use_pred else None)
+                pred_in=bf.pred if use_pred else None, residual=residual)
         if lin.result is not None:
             for h in self.hooks:
                 h(lin, lin.result)
@@ -390,30 +404,41 @@ class ProtectedViT(torch.nn.Module):
                 save(base, h, a)
                 self._lin(base, a, bf.qkv, bf, protect, inj, pred=True)
                 self._attention(bf)
+            fr = self.fused_residual
+            h2 = bf.h2 if fr else h  # the residual stream after proj
             if start <= base + 1:
                 if start == base + 1:
                     load(base + 1, h, bf.o)
                     bf.o_view = bf.o
                 save(base + 1, h, bf.o_view)
-                self._lin(base + 1, bf.o_view, bf.y, bf, protect, inj)
-                self._ln_into(base + 2, protect, bf, h, bf.y, *self._ln(2 * b + 1), h_out=h)
+                if fr:  # h2 = h + proj(o) stored by the GEMM, then the layer norm of h2 alone
+                    self._lin(base + 1, bf.o_view, h2, bf, protect, inj, residual=h)
+                    self._ln_into(base + 2, protect, bf, h2, None, *self._ln(2 * b + 1))
+                else:
+                    self._lin(base + 1, bf.o_view, bf.y, bf, protect, inj)
+                    self._ln_into(base + 2, protect, bf, h, bf.y, *self._ln(2 * b + 1), h_out=h)
             if start <= base + 2:
                 if start == base + 2:
-                    load(base + 2, h, a)
-                save(base + 2, h, a)
+                    load(base + 2, h2, a)
+                save(base + 2, h2, a)
                 self._lin(base + 2, a, bf.f, bf, protect, inj, pred=True)
                 if not self.fused_gelu:
                     bf.f.copy_(F.gelu(bf.f, approximate="tanh"))
             if start <= base + 3:
                 if start == base + 3:
-                    load(base + 3, h, bf.f)
-                save(base + 3, h, bf.f)
-                self._lin(base + 3, bf.f, bf.y, bf, protect, inj)
+                    load(base + 3, h2, bf.f)
+                save(base + 3, h2, bf.f)
                 nxt = base + 4 if b + 1 < c.depth else None  # the next qkv (the final norm feeds the head's cls rows)
-                if nxt is not None:
-                    self._ln_into(nxt, protect, bf, h, bf.y, *self._ln(2 * b + 2), h_out=h)
+                if fr:  # h = h2 + fc2(f) stored by the GEMM
+                    self._lin(base + 3, bf.f, h, bf, protect, inj, residual=h2)
+                    y_add = None
                 else:
-                    K.add_layernorm(h, bf.y, *self._ln(2 * b + 2), eps, ln_out=a, h_out=h)
+                    self._lin(base + 3, bf.f, bf.y, bf, protect, inj)
+                    y_add = bf.y
+                if nxt is not None:
+                    self._ln_into(nxt, protect, bf, h, y_add, *self._ln(2 * b + 2), h_out=h if y_add is not None else None)
+                else:
+                    K.add_layernorm(h, y_add, *self._ln(2 * b + 2), eps, ln_out=a, h_out=h if y_add is not None else None)
                     bf.pred_valid = False
         head = c.n_layers - 1
         if start == head:
