@@ -59,7 +59,7 @@ CONFIDENCE = 1.0 - 1e-9  # per-row checks: ~50k rows x 50 layers per step => kee
 
 # DRAM bytes (read + write) per protected launch, from `ncu --set full` captures of K1
 # (profiles/r02/full_{proj,fc2}.ncu-rep and SUMMARY.md; profiles/ does not travel to the box)
-NCU_DRAM_MB = {"qkv": 282.5, "proj": 115.4, "fc1": 372.3, "fc2": 383.1}  # profiles/r02/ncu_summaries (final)
+NCU_DRAM_MB = {"qkv": 284.3, "proj": 115.6, "fc1": 369.0, "fc2": 382.4}  # profiles/r02/ncu_summaries (final)
 
 
 def step_traffic_bytes() -> float:
