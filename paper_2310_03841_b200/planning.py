@@ -16,22 +16,31 @@ analysis.py:297-306).
 Here the counters come from the batched device campaign (`campaign.py`,
 all-reduced across ranks by K5), the model is a `ProtectedViT` (its GEMM list
 gives the MAC counts) and a plan is applied with `ProtectedViT.set_protected`.
-Selection: layers by decreasing vulnerability per unit cost until the target
-is met, then the most expensive picks the target can spare are dropped; the
+Selection follows the reference's rule and summation order (so plans and
+their float fields are the reference's bytes): walk the layers by decreasing
+vulnerability per unit cost; at every prefix also try completing it with the
+cheapest single layer that covers the rest; drop from each candidate the most
+expensive picks the target can spare; keep the cheapest candidate.  The
 exhaustive search (`method="exact"`, up to 20 candidates) is the optimality
 oracle of the tests.
+
+The same module serves the workbench CLI over the reference's toy models
+(`cli.py`): `compute_v_orig`, `layer_vulnerabilities`
+over a `CampaignResult`, the coverage curves and the checksum / duplication
+cost models of a `LayerSpec` (analysis.py:95-133,185-206,297-322).
 """
 
 from __future__ import annotations
 
 import json
-from dataclasses import asdict, dataclass
+from dataclasses import dataclass
 from itertools import combinations
 
 import numpy as np
 
-__all__ = ["LayerVulnerability", "ProtectionPlan", "layer_macs", "layer_vulnerabilities", "checksum_costs",
-           "select_layers"]
+__all__ = ["LayerVulnerability", "ProtectionPlan", "CoverageCurve", "layer_macs", "layer_vulnerabilities",
+           "checksum_costs", "select_layers", "compute_v_orig", "build_coverage_curve", "checksum_cost_model",
+           "duplication_cost_model", "model_totals"]
 
 
 @dataclass
@@ -43,8 +52,14 @@ class LayerVulnerability:
     v_layer: float
 
 
+_PLAN_FIELDS = ("scheme", "selected", "predicted_coverage", "compute_overhead", "memory_overhead",
+                "head_always_included")
+
+
 @dataclass
 class ProtectionPlan:
+    """A protected layer set and its predicted coverage / overheads (analysis.py:44-79)."""
+
     scheme: str
     selected: tuple[int, ...]
     predicted_coverage: float
@@ -52,10 +67,34 @@ class ProtectionPlan:
     memory_overhead: float
     head_always_included: bool
 
-    def to_json(self) -> str:
-        d = asdict(self)
+    def to_dict(self) -> dict:
+        d = {k: getattr(self, k) for k in _PLAN_FIELDS}
         d["selected"] = list(self.selected)
-        return json.dumps(d, indent=2, sort_keys=True)
+        return d
+
+    def to_json(self) -> str:
+        return json.dumps(self.to_dict(), indent=2, sort_keys=True)
+
+    @classmethod
+    def from_dict(cls, doc: dict) -> "ProtectionPlan":
+        kw = {k: doc[k] for k in _PLAN_FIELDS}
+        kw["selected"] = tuple(kw["selected"])
+        return cls(**kw)
+
+    @classmethod
+    def from_json(cls, text: str) -> "ProtectionPlan":
+        return cls.from_dict(json.loads(text))
+
+
+@dataclass
+class CoverageCurve:
+    """(cumulative overhead, cumulative coverage) as layers are added by value / cost, from (0, 0)."""
+
+    points: list[tuple[float, float]]
+    order: list[int]
+
+    def to_csv(self) -> str:
+        return "overhead,coverage\n" + "".join(f"{o!r},{c!r}\n" for o, c in self.points)
 
 
 def layer_macs(model) -> np.ndarray:
@@ -72,8 +111,36 @@ def checksum_costs(model) -> tuple[np.ndarray, np.ndarray]:
     return np.array(comp), np.array(mem)
 
 
+def compute_v_orig(model) -> np.ndarray:
+    """MAC share of every layer of a toy `ModelGraph`, summing to 1 (analysis.py:95-98)."""
+    from .model import mac_count
+
+    macs = np.array([mac_count(layer) for layer in model.layers], dtype=np.float64)
+    return macs / macs.sum()
+
+
+def _campaign_vulnerabilities(model, campaign) -> list[LayerVulnerability]:
+    """analysis.py:101-133 over a `CampaignResult`'s per-layer tallies."""
+    share = compute_v_orig(model)
+    tallies = campaign.layer_tallies()
+    out = []
+    for layer in model.layers:
+        t = tallies.get(layer.index)
+        if not t or t["injections"] == 0:
+            raise ValueError(f"no injection records for layer {layer.index}")
+        p = t["mismatches"] / t["injections"]
+        v = float(share[layer.index])
+        out.append(LayerVulnerability(layer.index, v, p, t["loss_delta_sum"] / t["injections"], v * p))
+    return out
+
+
 def layer_vulnerabilities(model, tally) -> list[LayerVulnerability]:
-    """V_orig, P_prop, Delta-loss and V_orig * P_prop per layer from a campaign's counters."""
+    """V_orig, P_prop, Delta-loss and V_orig * P_prop per layer.
+
+    `tally` is the device campaign's counters (`campaign.Tally`, model a
+    `ProtectedViT`) or a host `CampaignResult` (model a toy `ModelGraph`)."""
+    if hasattr(tally, "layer_tallies"):
+        return _campaign_vulnerabilities(model, tally)
     macs = layer_macs(model)
     share = macs / macs.sum()
     out = []
@@ -86,10 +153,54 @@ def layer_vulnerabilities(model, tally) -> list[LayerVulnerability]:
     return out
 
 
+def _ratio_order(v: np.ndarray, c: np.ndarray, items) -> list[int]:
+    """`items` by decreasing value / cost (zero cost first), then cheaper, then lower index
+    (analysis.py:136-140)."""
+    with np.errstate(divide="ignore", invalid="ignore"):  # zero costs: the np.where picks inf
+        r = np.where(c > 0, v / c, np.inf)
+    return sorted(items, key=lambda i: (-r[i], c[i], i))
+
+
+def _spare(v, c, need: float, picks: list[int]) -> list[int]:
+    """Drop the most expensive picks the target can spare (analysis.py:143-151)."""
+    kept = list(picks)
+    got = sum(float(v[i]) for i in kept)
+    for i in sorted(kept, key=lambda j: (-c[j], j)):
+        if got - float(v[i]) >= need:
+            kept.remove(i)
+            got -= float(v[i])
+    return kept
+
+
+def _greedy(v, c, need: float, free: list[int]) -> list[int]:
+    """Ratio-ordered prefixes, each also completed by the cheapest single layer covering the
+    rest, spared, cheapest kept (analysis.py:154-182)."""
+    walk = _ratio_order(v, c, free)
+    cands: list[list[int]] = []
+    prefix: list[int] = []
+    got = 0.0
+    for j in range(len(walk) + 1):
+        rest = need - got
+        if rest <= 0:
+            cands.append(list(prefix))
+            break
+        cover = [i for i in walk[j:] if float(v[i]) >= rest]
+        if cover:
+            cands.append(prefix + [min(cover, key=lambda i: (c[i], i))])
+        if j < len(walk):
+            prefix.append(walk[j])
+            got += float(v[walk[j]])
+    if not cands:
+        raise ValueError("coverage target unreachable")
+    spared = [_spare(v, c, need, cand) for cand in cands]
+    return min(spared, key=lambda s: (sum(float(c[i]) for i in s), len(s), tuple(sorted(s))))
+
+
 def select_layers(vulns, costs, target_coverage: float, *, head_index: int | None = None, method: str = "greedy",
                   total_compute: float | None = None, memory_costs=None, total_memory: float | None = None,
                   scheme: str = "checksum") -> ProtectionPlan:
-    """Cheapest layer set whose vulnerability reaches target_coverage of the total (head forced in)."""
+    """Cheapest layer set whose vulnerability reaches target_coverage of the total, head forced
+    in (analysis.py:213-290; same sums in the same order, so the plan's floats are the reference's)."""
     v = np.asarray(vulns, dtype=np.float64)
     c = np.asarray(costs, dtype=np.float64)
     if not 0.0 < target_coverage <= 1.0:
@@ -99,42 +210,80 @@ def select_layers(vulns, costs, target_coverage: float, *, head_index: int | Non
     total = float(v.sum())
     if total <= 0:
         raise ValueError("total vulnerability is zero")
-    forced = [] if head_index is None else [head_index]
-    need = target_coverage * total * (1.0 - 1e-12)
+    forced = set() if head_index is None else {head_index}
     free = [i for i in range(len(v)) if i not in forced]
-    base = float(sum(v[i] for i in forced))
     if method == "greedy":
-        ratio = {i: (v[i] / c[i] if c[i] > 0 else np.inf) for i in free}
-        chosen, got = [], base
-        for i in sorted(free, key=lambda j: (-ratio[j], c[j], j)):
-            if got >= need:
-                break
-            chosen.append(i)
-            got += float(v[i])
-        if got < need:
-            raise ValueError(f"target coverage {target_coverage} unreachable")
-        for i in sorted(chosen, key=lambda j: (-c[j], j)):  # drop what the target can spare
-            if got - float(v[i]) >= need:
-                chosen.remove(i)
-                got -= float(v[i])
-        picked = chosen
+        chosen = set(forced)
+        got = sum(float(v[i]) for i in forced)
+        need = target_coverage * total - got - 1e-12 * total
+        if need > 0:
+            picks = _greedy(v, c, need, free)
+            chosen |= set(picks)
+            got += sum(float(v[i]) for i in picks)
+        if got / total < target_coverage - 1e-12:
+            raise ValueError(f"target coverage {target_coverage} unreachable (max {got / total})")
     elif method == "exact":
         if len(v) > 20:
             raise ValueError("exact selection is limited to 20 layers")
+        need = target_coverage * total - sum(float(v[i]) for i in forced)
         best = None
         for r in range(len(free) + 1):
             for combo in combinations(free, r):
-                cov = base + float(sum(v[i] for i in combo))
-                if cov >= need:
-                    key = (float(sum(c[i] for i in combo)), -cov, combo)
+                cost, cov = float(sum(c[i] for i in combo)), float(sum(v[i] for i in combo))
+                if cov >= need - 1e-12 * total:
+                    key = (cost, -cov, combo)
                     best = key if best is None or key < best else best
         if best is None:
             raise ValueError(f"target coverage {target_coverage} unreachable")
-        picked = list(best[2])
+        chosen = set(forced) | set(best[2])
+        got = sum(float(v[i]) for i in chosen)
     else:
         raise ValueError(f"unknown selection method {method!r}")
-    sel = tuple(sorted(set(forced) | set(picked)))
+    sel = tuple(sorted(chosen))
     cost = float(sum(c[i] for i in sel))
     mem = float(sum(memory_costs[i] for i in sel)) / total_memory if (memory_costs is not None and total_memory) else 0.0
-    return ProtectionPlan(scheme, sel, float(sum(v[i] for i in sel)) / total,
-                          cost / total_compute if total_compute else cost, mem, head_index is not None)
+    return ProtectionPlan(scheme, sel, got / total, cost / total_compute if total_compute else cost, mem,
+                          head_index is not None)
+
+
+def build_coverage_curve(vulns, costs, scheme: str = "checksum") -> CoverageCurve:
+    """Cumulative coverage against cumulative overhead, layers added by value / cost; coverage
+    normalised over the layers given (analysis.py:185-206)."""
+    v = np.asarray(vulns, dtype=np.float64)
+    c = np.asarray(costs, dtype=np.float64)
+    if v.shape != c.shape or v.ndim != 1:
+        raise ValueError("vulns and costs must be equal-length vectors")
+    if (c < 0).any():
+        raise ValueError("costs must be nonnegative")
+    total = v.sum()
+    order = _ratio_order(v, c, range(len(v)))
+    pts = [(0.0, 0.0)]
+    oc = ov = 0.0
+    for i in order:
+        oc += float(c[i])
+        ov += float(v[i])
+        pts.append((oc, ov / total if total > 0 else 0.0))
+    return CoverageCurve(points=pts, order=order)
+
+
+def checksum_cost_model(layer) -> tuple[float, float]:
+    """(flops, memory elements) of checking one toy layer: input and output row sums plus the
+    checksum dot product per token; the weight checksum plus two online vectors (analysis.py:297-306)."""
+    return float(layer.tokens * (2 * layer.in_dim + layer.out_dim)), float(layer.in_dim + 2 * layer.tokens)
+
+
+def duplication_cost_model(layer) -> tuple[float, float]:
+    """(flops, memory elements) of running one toy layer twice (analysis.py:309-313)."""
+    from .model import mac_count
+
+    return (float(2 * mac_count(layer)),
+            float(layer.in_dim * layer.out_dim + layer.out_dim + layer.tokens * layer.out_dim))
+
+
+def model_totals(model) -> tuple[float, float]:
+    """(forward flops, resident elements) of a toy model (analysis.py:316-322)."""
+    from .model import mac_count
+
+    return (float(sum(2 * mac_count(layer) for layer in model.layers)),
+            float(sum(layer.in_dim * layer.out_dim + layer.out_dim + layer.tokens * layer.out_dim
+                      for layer in model.layers)))

@@ -43,3 +43,33 @@ def test_vit_b16_cost_model():
     assert len(macs) == 50 and abs(2 * macs.sum() - 33.70e9) < 0.01e9  # protected GEMM flops / image
     # checksum work relative to the GEMM: 1/N + 1/(2K) per layer
     assert comp[2] / (2 * macs[2]) == pytest.approx(1 / 768 + 1 / (2 * 768))
+
+
+def test_planning_matches_reference_golden():
+    """select_layers (greedy / exact, cost and memory totals) and build_coverage_curve give the
+    reference's bytes on 60 seeded cases (tests/golden/planning.json, written by the reference)."""
+    import json
+    import warnings
+    from pathlib import Path
+
+    from paper_2310_03841_b200.planning import build_coverage_curve
+
+    cases = json.loads((Path(__file__).parent / "golden" / "planning.json").read_text())
+    for case in cases:
+        v, c, mem = np.array(case["v"]), np.array(case["c"]), np.array(case["mem"])
+        for method in ("greedy", "exact"):
+            want = case[method]
+            if isinstance(want, dict):
+                with pytest.raises(ValueError) as exc:
+                    select_layers(v, c, case["target"], head_index=case["head"], method=method,
+                                  total_compute=case["total_compute"], memory_costs=mem,
+                                  total_memory=case["total_memory"])
+                assert str(exc.value) == want["error"]
+            else:
+                got = select_layers(v, c, case["target"], head_index=case["head"], method=method,
+                                    total_compute=case["total_compute"], memory_costs=mem,
+                                    total_memory=case["total_memory"])
+                assert got.to_json() == want
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)  # 0 / 0 ratios, as in the reference
+            assert build_coverage_curve(v, c).to_csv() == case["curve"]
