@@ -106,3 +106,13 @@ def test_tensor_engine_moves_only_low_bits(tmp_path):
     for rg, rw in zip(g, w):
         if rw[1]:
             assert abs(float(rg[1]) - float(rw[1])) <= 1e-6 + 1e-3 * abs(float(rw[1]))
+
+
+def test_inject_with_workers_matches_single_process(tmp_path):
+    """--workers 2 runs the float toy's layers in spawned worker processes (each its own CUDA
+    context); the campaign CSV is the reference's single-process bytes."""
+    cfg = GOLDEN / "fp16_toy" / "config.json"
+    assert main(["profile", "--config", str(cfg), "--out", str(tmp_path)]) == 0
+    assert main(["inject", "--config", str(cfg), "--out", str(tmp_path), "--workers", "2"]) == 0
+    for a in ("campaign.csv", "campaign_summary.json"):
+        assert (tmp_path / a).read_bytes() == (GOLDEN / "fp16_toy" / a).read_bytes(), a
