@@ -187,14 +187,16 @@ __global__ void __launch_bounds__(256, ln_min_blocks(CH * Vec<T>::N)) add_layern
 }
 
 // The plain layer norm (no residual add, no predicted sums: the ViT's norms once the GEMMs
-// store the residual update) as a persistent grid: each warp walks rows row0, row0 + stride, ...
-// and loads its next row before reducing the current one, so every warp keeps two rows in
-// flight.  Same sums in the same order as add_layernorm_kernel (identical bytes); ViT-B b256
-// (50432 x 768 bf16) 47.5 -> 44.5 us, against 33.3 us for a plain copy of the same bytes
-// (tools/ab_ln.py, tools/ln_ref.py).  More resident warps instead (the row packed in registers,
-// six or eight blocks per SM) measured slower: 54 / 63 us.
+// store the residual update) as a persistent grid: each warp walks rows row0, row0 + stride, ...,
+// keeps its lanes' affine parameters in registers (loaded once instead of once per row: five
+// times the row's own bytes of L1 traffic) and loads its next row before reducing the current
+// one.  Same sums in the same order as add_layernorm_kernel (identical bytes).  ViT-B b256
+// (50432 x 768 bf16): 47.5 -> 43 us, against 33.3 us for a plain copy of the same bytes
+// (tools/ab_ln.py, tools/ln_ref.py).  Slower alternatives measured: more resident warps with the
+// row kept packed (54 / 63 us at six / eight blocks per SM), rows staged through a per-warp TMA
+// ring in shared memory (50-63 us for 4-12 rows in flight per warp).
 #ifndef GG_LN_STREAM_BPS
-#define GG_LN_STREAM_BPS 3  // resident 256-thread blocks per SM (measured: 2 -> 46, 3 -> 44.5, 4 -> 46 us)
+#define GG_LN_STREAM_BPS 2  // resident 256-thread blocks per SM (the affine registers: 76 per thread)
 #endif
 template <typename T, int CH>
 __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel(const T* __restrict__ h, int64_t rows,
@@ -206,6 +208,17 @@ __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel
   const int64_t stride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   uint4 cur[CH], nxt[CH];
+  float gr[CH][V], br[CH][V];  // this lane's affine parameters, the same for every row it walks
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+#pragma unroll
+    for (int i = 0; i < V; i += 4) {
+      const int col = (c * 32 + lane) * V + i;
+      const float4 g4 = __ldg(reinterpret_cast<const float4*>(gamma + col));
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(beta + col));
+      gr[c][i] = g4.x; gr[c][i + 1] = g4.y; gr[c][i + 2] = g4.z; gr[c][i + 3] = g4.w;
+      br[c][i] = b4.x; br[c][i + 1] = b4.y; br[c][i + 2] = b4.z; br[c][i + 3] = b4.w;
+    }
   if (row < rows) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) cur[c] = *reinterpret_cast<const uint4*>(h + row * D + (c * 32 + lane) * V);
@@ -247,14 +260,7 @@ __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel
       float v[V], o[V];
       Vec<T>::load(&cur[c], v);
 #pragma unroll
-      for (int i = 0; i < V; i += 4) {
-        const float4 g4 = __ldg(reinterpret_cast<const float4*>(gamma + col + i));
-        const float4 b4 = __ldg(reinterpret_cast<const float4*>(beta + col + i));
-        o[i] = fmaf((v[i] - mean) * rstd, g4.x, b4.x);
-        o[i + 1] = fmaf((v[i + 1] - mean) * rstd, g4.y, b4.y);
-        o[i + 2] = fmaf((v[i + 2] - mean) * rstd, g4.z, b4.z);
-        o[i + 3] = fmaf((v[i + 3] - mean) * rstd, g4.w, b4.w);
-      }
+      for (int i = 0; i < V; ++i) o[i] = fmaf((v[i] - mean) * rstd, gr[c][i], br[c][i]);
       Vec<T>::store(ln_out + row * D + col, o);
     }
 #pragma unroll
