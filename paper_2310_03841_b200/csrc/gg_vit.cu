@@ -198,11 +198,13 @@ __global__ void __launch_bounds__(256, ln_min_blocks(CH * Vec<T>::N)) add_layern
 #ifndef GG_LN_STREAM_BPS
 #define GG_LN_STREAM_BPS 2  // resident 256-thread blocks per SM (the affine registers: 76 per thread)
 #endif
-template <typename T, int CH>
+template <typename T, int CH, bool PRED>
 __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel(const T* __restrict__ h, int64_t rows,
                                                                                  int D, const float* __restrict__ gamma,
                                                                                  const float* __restrict__ beta,
-                                                                                 float eps, T* __restrict__ ln_out) {
+                                                                                 float eps, T* __restrict__ ln_out,
+                                                                                 const float* __restrict__ w_pred,
+                                                                                 unsigned long long* __restrict__ pred_out) {
   constexpr int V = Vec<T>::N;
   const int lane = threadIdx.x & 31;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -219,6 +221,16 @@ __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel
       gr[c][i] = g4.x; gr[c][i + 1] = g4.y; gr[c][i + 2] = g4.z; gr[c][i + 3] = g4.w;
       br[c][i] = b4.x; br[c][i + 1] = b4.y; br[c][i + 2] = b4.z; br[c][i + 3] = b4.w;
     }
+  float wr[PRED ? CH : 1][V];  // the consumer's checksum vector at this lane's columns (PRED)
+  if constexpr (PRED) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+      for (int i = 0; i < V; i += 4) {
+        const float4 w4 = __ldg(reinterpret_cast<const float4*>(w_pred + (c * 32 + lane) * V + i));
+        wr[c][i] = w4.x; wr[c][i + 1] = w4.y; wr[c][i + 2] = w4.z; wr[c][i + 3] = w4.w;
+      }
+  }
   if (row < rows) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) cur[c] = *reinterpret_cast<const uint4*>(h + row * D + (c * 32 + lane) * V);
@@ -254,6 +266,7 @@ __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
     const float rstd = rsqrtf(q / static_cast<float>(D) + eps);
+    float p = 0.f;
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const int col = (c * 32 + lane) * V;
@@ -261,7 +274,21 @@ __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel
       Vec<T>::load(&cur[c], v);
 #pragma unroll
       for (int i = 0; i < V; ++i) o[i] = fmaf((v[i] - mean) * rstd, gr[c][i], br[c][i]);
-      Vec<T>::store(ln_out + row * D + col, o);
+      if constexpr (PRED) {  // add_layernorm_kernel's predicted sum: the same products, the same order
+        uint4 packed;
+        Vec<T>::store(&packed, o);
+        Vec<T>::load(&packed, o);
+        *reinterpret_cast<uint4*>(ln_out + row * D + col) = packed;
+#pragma unroll
+        for (int i = 0; i < V; ++i) p = fmaf(o[i], wr[c][i], p);
+      } else {
+        Vec<T>::store(ln_out + row * D + col, o);
+      }
+    }
+    if constexpr (PRED) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+      if (lane == 0) pred_out[row] = static_cast<unsigned long long>(__float_as_uint(p));
     }
 #pragma unroll
     for (int c = 0; c < CH; ++c) cur[c] = nxt[c];
@@ -291,10 +318,13 @@ int launch_add_ln_t(const void* h, const void* y, int64_t rows, int D, const flo
   const T* yp = static_cast<const T*>(y);
   T* ho = static_cast<T*>(h_out);
   T* lo = static_cast<T*>(ln_out);
-  if (y == nullptr && w_pred == nullptr && ch == 3) {  // the ViT-B / Swin-B stage-1 width
+  if (y == nullptr && ch == 3) {  // the ViT-B / Swin-B stage-1 width
     const int64_t want = (rows + 7) / 8;
     const unsigned g = static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * GG_LN_STREAM_BPS));
-    layernorm_stream_kernel<T, 3><<<g, 256, 0, s>>>(hp, rows, D, gamma, beta, eps, lo);
+    if (w_pred != nullptr)
+      layernorm_stream_kernel<T, 3, true><<<g, 256, 0, s>>>(hp, rows, D, gamma, beta, eps, lo, w_pred, pred_out);
+    else
+      layernorm_stream_kernel<T, 3, false><<<g, 256, 0, s>>>(hp, rows, D, gamma, beta, eps, lo, nullptr, nullptr);
     return check_launch("add_layernorm");
   }
   switch (ch) {

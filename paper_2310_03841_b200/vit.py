@@ -264,7 +264,9 @@ class ProtectedViT(torch.nn.Module):
         self.hooks = []  # callables (layer, result) after every protected launch (calibration)
         # Optionally the layer norms that feed qkv / fc1 also form those launches' predicted row
         # sums (pred_in), so K1's checksum warps hold no pipeline stage there.  Measured on ViT-B
-        # b256: K1 qkv / fc1 -6 / -8 us per launch, the layer norm +9 us: a wash, so off by default.
+        # b256: K1 qkv / fc1 -6 / -8 us per launch against the layer norm's extra work; with the
+        # persistent layer norm (checksum vector in registers) still a wash (+0.8% / -0.9% in two
+        # alternating runs, tools/pred_model_ab.py), so off by default.
         self.producer_pred = False
 
     # ------------------------------------------------------------- plumbing
