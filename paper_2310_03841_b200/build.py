@@ -89,7 +89,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
 def build_variant(name: str, defines: list[str]) -> Path:
     """Diagnostics / A-B build with extra preprocessor defines, linked to
-    _build/libgemmguard_b200_<name>.so; never loaded by the product (select it
+    _variants/libgemmguard_b200_<name>.so; never loaded by the product (select it
     with $GEMMGUARD_LIB)."""
     BUILD.mkdir(exist_ok=True)
     objs = []
@@ -119,7 +119,7 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--trace", action="store_true", help="also build the diagnostics library")
     ap.add_argument("--variant", nargs="+", metavar=("NAME", "DEFINE"),
-                    help="also build _build/libgemmguard_b200_NAME.so with -DDEFINE for each DEFINE")
+                    help="also build _variants/libgemmguard_b200_NAME.so with -DDEFINE for each DEFINE")
     a = ap.parse_args()
     print(build(force=a.force, verbose=True))
     if a.trace:

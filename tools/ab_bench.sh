@@ -2,7 +2,7 @@
 rounds=$1; shift
 for r in $(seq $rounds); do
   for v in "$@"; do
-    if [ "$v" != cur ]; then export GEMMGUARD_LIB=paper_2310_03841_b200/_build/libgemmguard_b200_$v.so; else unset GEMMGUARD_LIB; fi
+    if [ "$v" != cur ]; then export GEMMGUARD_LIB=paper_2310_03841_b200/_variants/libgemmguard_b200_$v.so; else unset GEMMGUARD_LIB; fi
     timeout 400 python bench.py --no-cpu-baseline 2>/dev/null | tail -1 | python -c "
 import sys, json
 d = json.loads(sys.stdin.read())

@@ -3,7 +3,7 @@
 # usage: bash tools/ab_ncu.sh "M N K" variant...   (variant "cur" = the in-tree library)
 shape=$1; shift
 for v in "$@"; do
-  if [ "$v" != cur ]; then export GEMMGUARD_LIB=paper_2310_03841_b200/_build/libgemmguard_b200_$v.so; else unset GEMMGUARD_LIB; fi
+  if [ "$v" != cur ]; then export GEMMGUARD_LIB=paper_2310_03841_b200/_variants/libgemmguard_b200_$v.so; else unset GEMMGUARD_LIB; fi
   ncu --metrics gpu__time_duration.sum -k regex:gg_protected --csv python tools/prof_one.py $shape ${DT:-bf16} 2>/dev/null \
     | python -c "
 import sys, csv

@@ -1,4 +1,4 @@
-"""(Use the diagnostics build for GG_DEBUG switches: GEMMGUARD_LIB=paper_2310_03841_b200/_build/libgemmguard_b200_diag.so)
+"""(Use the diagnostics build for GG_DEBUG switches: GEMMGUARD_LIB=paper_2310_03841_b200/_variants/libgemmguard_b200_diag.so)
 Protected vs unprotected timing of one shape: each arm is a CUDA graph of G launches, and
 the two graphs are replayed alternately R times (both arms see the same clock / power-cap
 state; no host launch overhead).  GG_DEBUG selects the diagnostic switches (read once per

@@ -1,6 +1,6 @@
 """Per-tile role timeline of one protected GEMM from the GG_TRACE library.
 
-    GEMMGUARD_LIB=paper_2310_03841_b200/_build/libgemmguard_b200_trace.so \
+    GEMMGUARD_LIB=paper_2310_03841_b200/_variants/libgemmguard_b200_trace.so \
         python tools/trace_tiles.py M N K [protect] [bf16|f16|tf32]
 """
 import ctypes, os, sys
