@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(256, ln_min_blocks(CH * Vec<T>::N)) add_layern
 // keeps its lanes' affine parameters in registers (loaded once instead of once per row: five
 // times the row's own bytes of L1 traffic) and loads its next row before reducing the current
 // one.  Same sums in the same order as add_layernorm_kernel (identical bytes).  ViT-B b256
-// (50432 x 768 bf16): 47.5 -> 43 us, against 33.3 us for a plain copy of the same bytes
+// (50432 x 768 bf16): 47.5 -> 43 us, against 33.3 us for a plain copy of the same bytes; ViT-L
+// width (1024, no prefetch: 56 bytes of spill for the affine registers): 79 -> 52.5 us
 // (tools/ab_ln.py, tools/ln_ref.py).  Slower alternatives measured: more resident warps with the
 // row kept packed (54 / 63 us at six / eight blocks per SM), rows staged through a per-warp TMA
 // ring in shared memory (50-63 us for 4-12 rows in flight per warp).
@@ -209,7 +210,8 @@ __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel
   const int lane = threadIdx.x & 31;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  uint4 cur[CH], nxt[CH];
+  constexpr bool PF = CH <= 3;  // prefetch the next row (wider rows: the registers go to the affine parameters)
+  uint4 cur[CH], nxt[PF ? CH : 1];
   float gr[CH][V], br[CH][V];  // this lane's affine parameters, the same for every row it walks
 #pragma unroll
   for (int c = 0; c < CH; ++c)
@@ -237,9 +239,11 @@ __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel
   }
   for (; row < rows; row += stride) {
     const int64_t nrow = row + stride;
-    if (nrow < rows) {
+    if constexpr (PF) {
+      if (nrow < rows) {
 #pragma unroll
-      for (int c = 0; c < CH; ++c) nxt[c] = *reinterpret_cast<const uint4*>(h + nrow * D + (c * 32 + lane) * V);
+        for (int c = 0; c < CH; ++c) nxt[c] = *reinterpret_cast<const uint4*>(h + nrow * D + (c * 32 + lane) * V);
+      }
     }
     float s = 0.f;
 #pragma unroll
@@ -290,8 +294,13 @@ __global__ void __launch_bounds__(256, GG_LN_STREAM_BPS) layernorm_stream_kernel
       for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
       if (lane == 0) pred_out[row] = static_cast<unsigned long long>(__float_as_uint(p));
     }
+    if constexpr (PF) {
 #pragma unroll
-    for (int c = 0; c < CH; ++c) cur[c] = nxt[c];
+      for (int c = 0; c < CH; ++c) cur[c] = nxt[c];
+    } else if (nrow < rows) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) cur[c] = *reinterpret_cast<const uint4*>(h + nrow * D + (c * 32 + lane) * V);
+    }
   }
 }
 
@@ -318,13 +327,20 @@ int launch_add_ln_t(const void* h, const void* y, int64_t rows, int D, const flo
   const T* yp = static_cast<const T*>(y);
   T* ho = static_cast<T*>(h_out);
   T* lo = static_cast<T*>(ln_out);
-  if (y == nullptr && ch == 3) {  // the ViT-B / Swin-B stage-1 width
+  if (y == nullptr && (ch == 3 || ch == 4)) {  // ViT-B (768) and ViT-L (1024) widths at 16 bits
     const int64_t want = (rows + 7) / 8;
     const unsigned g = static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * GG_LN_STREAM_BPS));
-    if (w_pred != nullptr)
-      layernorm_stream_kernel<T, 3, true><<<g, 256, 0, s>>>(hp, rows, D, gamma, beta, eps, lo, w_pred, pred_out);
-    else
-      layernorm_stream_kernel<T, 3, false><<<g, 256, 0, s>>>(hp, rows, D, gamma, beta, eps, lo, nullptr, nullptr);
+    if (ch == 3) {
+      if (w_pred != nullptr)
+        layernorm_stream_kernel<T, 3, true><<<g, 256, 0, s>>>(hp, rows, D, gamma, beta, eps, lo, w_pred, pred_out);
+      else
+        layernorm_stream_kernel<T, 3, false><<<g, 256, 0, s>>>(hp, rows, D, gamma, beta, eps, lo, nullptr, nullptr);
+    } else {
+      if (w_pred != nullptr)
+        layernorm_stream_kernel<T, 4, true><<<g, 256, 0, s>>>(hp, rows, D, gamma, beta, eps, lo, w_pred, pred_out);
+      else
+        layernorm_stream_kernel<T, 4, false><<<g, 256, 0, s>>>(hp, rows, D, gamma, beta, eps, lo, nullptr, nullptr);
+    }
     return check_launch("add_layernorm");
   }
   switch (ch) {

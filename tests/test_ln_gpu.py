@@ -1,4 +1,4 @@
-"""The persistent layer norm (gg_add_layernorm without a residual add at D = 768, the ViT-B width)
+"""The persistent layer norm (gg_add_layernorm without a residual add at D = 768 / 1024, the ViT-B / ViT-L widths)
 against the one-pass kernel it replaces: adding a zero residual routes the same rows through
 add_layernorm_kernel, whose sums are the same in the same order, so the normalised rows and the
 consumer's predicted sums must be bit-identical; plus torch fp32 within bf16 / fp16 rounding, and
@@ -18,8 +18,8 @@ from paper_2310_03841_b200 import kernels as K  # noqa: E402
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("rows", [1, 7, 1001, 50432])
 @pytest.mark.parametrize("pred", [False, True])
-def test_stream_layernorm_matches_the_one_pass_kernel(dtype, rows, pred):
-    D = 768
+@pytest.mark.parametrize("D", [768, 1024])
+def test_stream_layernorm_matches_the_one_pass_kernel(dtype, rows, pred, D):
     g = torch.Generator(device="cuda").manual_seed(rows + 3 * pred)
     h = (2.0 * torch.randn(rows, D, device="cuda", generator=g) + 0.5).to(dtype)
     gm = 1.0 + 0.1 * torch.randn(D, device="cuda", generator=g)
