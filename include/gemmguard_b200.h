@@ -339,7 +339,8 @@ GG_API int gg_int_finish(const int32_t* Y, int64_t B, int64_t T, int64_t N, int6
  * pass: if y != NULL, h_out = round(h + y) (h_out may alias h); then
  * ln_out = LN(h_out or h) * gamma + beta with fp32 statistics over rows of D
  * (D a multiple of 32 x 16 bytes up to 8 such chunks per lane; dtype
- * GG_BF16, GG_F16 or GG_F32; 16-byte aligned, contiguous rows). */
+ * GG_BF16, GG_F16 or GG_F32; 16-byte aligned, contiguous rows).  ln_out must
+ * not alias h, y or h_out (GG_EINVAL). */
 GG_API int gg_add_layernorm(int32_t dtype, const void* h, const void* y, int64_t rows, int64_t D,
                             const float* gamma, const float* beta, float eps, void* h_out,
                             void* ln_out, const float* w_pred, uint64_t* pred_out, void* stream);

@@ -321,6 +321,8 @@ int launch_add_ln_t(const void* h, const void* y, int64_t rows, int D, const flo
                     cudaStream_t s) {
   constexpr int V = Vec<T>::N;
   if (D % (32 * V) != 0) return fail(GG_EUNSUPPORTED, "add_layernorm: D must be a multiple of 32 x 16 bytes");
+  if (ln_out == h || (y != nullptr && ln_out == y) || (h_out != nullptr && ln_out == h_out))
+    return fail(GG_EINVAL, "add_layernorm: ln_out must not alias h, y or h_out");
   const int ch = D / (32 * V);
   const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
   const T* hp = static_cast<const T*>(h);

@@ -44,3 +44,12 @@ def test_stream_layernorm_matches_the_one_pass_kernel(dtype, rows, pred, D):
     ref = torch.nn.functional.layer_norm(h.float(), (D,), gm, bt, 1e-6)
     ulp = 2.0**-7 if dtype == torch.bfloat16 else 2.0**-10
     assert bool(((a1.float() - ref).abs() <= ulp * ref.abs() + 1e-3).all())
+
+
+def test_layernorm_output_must_not_alias_its_input():
+    h = torch.randn(16, 768, device="cuda").to(torch.bfloat16)
+    gm, bt = torch.ones(768, device="cuda"), torch.zeros(768, device="cuda")
+    with pytest.raises(ValueError, match="alias"):
+        K.add_layernorm(h, None, gm, bt, 1e-6, ln_out=h)
+    with pytest.raises(ValueError, match="alias"):
+        K.add_layernorm(h, torch.zeros_like(h), gm, bt, 1e-6, ln_out=h, h_out=h)
